@@ -1,0 +1,466 @@
+// Device build of the gridding matrices (K12) and host-side deapodization.
+//
+// Restates gridding.py:84-195 (build_coo -> prune -> coo_to_csr) and
+// geometry.py:146-272 (kernel, kernel transform, deapodization) for the
+// device index convention (row-major grid m = gy*n_x + gx, sample
+// s = t*n_p + j).  Structural decisions (rint ties, kernel support, border,
+// Nyquist ring, in-bounds) are evaluated in IEEE double with explicit
+// round-to-nearest intrinsics so they reproduce the reference's numpy
+// evaluation exactly; S^H comes out in sample order with stencil-ordered
+// columns, S is obtained by a stable radix sort on the grid row.
+#include "sptb_internal.cuh"
+
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <vector>
+
+namespace sptb {
+
+namespace {
+
+struct BuildArgs {
+    int P, T, X, Y, W, family;
+    double beta, sigma, i0beta, thr;
+    const double* ct;     // cos(theta), device
+    const double* st;     // sin(theta), device
+    const double2* ramp;  // per detector bin phase (mirrored bins conjugated)
+};
+
+__device__ __forceinline__ double signed_freq(int j, int P) {
+    const int h = P / 2;
+    return (double)(((j + h) % P) - h);
+}
+
+// kernel_eval (geometry.py:146-161)
+__device__ double kern(const BuildArgs& a, double t) {
+    const double half = a.W * 0.5;
+    if (!(fabs(t) < half)) return 0.0;
+    if (a.family == SPTB_KERNEL_KB) {
+        const double q = __ddiv_rn(__dmul_rn(2.0, t), (double)a.W);
+        const double r = fmax(__dsub_rn(1.0, __dmul_rn(q, q)), 0.0);
+        return cyl_bessel_i0(a.beta * sqrt(r)) / a.i0beta;
+    }
+    const double z = t / a.sigma;
+    return exp(-0.5 * z * z);
+}
+
+// nearest node + fractional offset with negative-frequency mirroring
+// (gridding.py:100-121; polar_coords geometry.py:202-215)
+__device__ void sample_base(const BuildArgs& a, int t, int j, double& rx, double& ry,
+                            double& fx, double& fy) {
+    const double pj = signed_freq(j, a.P);
+    const bool nyq = (a.P % 2 == 0) && (j == a.P / 2);
+    const bool neg = pj < 0 && !nyq;
+    const int jj = neg ? (a.P - j) % a.P : j;
+    const double p = signed_freq(jj, a.P);
+    const double px = __dadd_rn(__dmul_rn(a.ct[t], p), a.X / 2.0);
+    const double py = __dadd_rn(__dmul_rn(a.st[t], p), a.Y / 2.0);
+    rx = rint(px);
+    ry = rint(py);
+    fx = __dsub_rn(px, rx);
+    fy = __dsub_rn(py, ry);
+    if (neg) {
+        rx = __dsub_rn((double)a.X, rx);
+        ry = __dsub_rn((double)a.Y, ry);
+        fx = -fx;
+        fy = -fy;
+    }
+}
+
+// One stencil entry: returns true when kept; sets grid row (C order) and value.
+__device__ bool entry(const BuildArgs& a, int t, int j, double rx, double ry, double fx,
+                      double fy, int si, int sj, int& m, double2& v) {
+    const int h = a.W / 2;
+    const int sx = si - h, sy = sj - h;
+    const long long gx = (long long)rx + sx, gy = (long long)ry + sy;
+    if (gx < 0 || gx >= a.X || gy < 0 || gy >= a.Y) return false;
+    if (gx == 0 || gy == 0) return false;                      // border (:136-137)
+    if ((a.P % 2 == 0) && j == a.P / 2) return false;           // Nyquist (:138-140)
+    const double kx = kern(a, __dsub_rn(fx, (double)sx));
+    const double ky = kern(a, __dsub_rn(fy, (double)sy));
+    const double wgt = kx * ky * ((((gx + gy) % 2) == 0) ? 1.0 : -1.0);
+    const double2 r = a.ramp[j];
+    v = make_double2(wgt * r.x, wgt * r.y);
+    if (!(hypot(v.x, v.y) > a.thr)) return false;               // prune (:159-163)
+    m = (int)(gy * a.X + gx);
+    return true;
+}
+
+__global__ void k_count(BuildArgs a, int* cnt) {
+    const long long N = (long long)a.T * a.P;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < N;
+         s += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(s / a.P), j = (int)(s % a.P);
+        double rx, ry, fx, fy;
+        sample_base(a, t, j, rx, ry, fx, fy);
+        int c = 0;
+        for (int si = 0; si < a.W; ++si)
+            for (int sj = 0; sj < a.W; ++sj) {
+                int m;
+                double2 v;
+                c += entry(a, t, j, rx, ry, fx, fy, si, sj, m, v) ? 1 : 0;
+            }
+        cnt[s] = c;
+    }
+}
+
+// S^H row s: columns m (stencil order), values conj(v)  (gridding.py:179)
+template <typename C>
+__global__ void k_fill(BuildArgs a, const int* rp, int* col, C* val, int* ent_s) {
+    const long long N = (long long)a.T * a.P;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < N;
+         s += (long long)gridDim.x * blockDim.x) {
+        const int t = (int)(s / a.P), j = (int)(s % a.P);
+        double rx, ry, fx, fy;
+        sample_base(a, t, j, rx, ry, fx, fy);
+        int o = rp[s];
+        for (int si = 0; si < a.W; ++si)
+            for (int sj = 0; sj < a.W; ++sj) {
+                int m;
+                double2 v;
+                if (entry(a, t, j, rx, ry, fx, fy, si, sj, m, v)) {
+                    col[o] = m;
+                    C c;
+                    c.x = v.x;
+                    c.y = -v.y;
+                    val[o] = c;
+                    ent_s[o] = (int)s;
+                    ++o;
+                }
+            }
+    }
+}
+
+__global__ void k_iota(int* v, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        v[i] = (int)i;
+}
+
+__global__ void k_row_hist(const int* keys, long long n, int* cnt) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        atomicAdd(cnt + keys[i], 1);
+}
+
+template <typename C>
+__global__ void k_gather_S(const int* perm, const int* ent_s, const C* shv, int* col, C* val,
+                           long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = perm[i];
+        col[i] = ent_s[k];
+        C v = shv[k];
+        v.y = -v.y;
+        val[i] = v;
+    }
+}
+
+int grid_of(long long n) {
+    long long g = (n + 255) / 256;
+    return (int)(g < 148LL * 64 ? (g > 0 ? g : 1) : 148LL * 64);
+}
+
+template <typename C>
+int build_typed(sptb_plan* p, const BuildArgs& a) {
+    cudaStream_t st = p->stream;
+    const long long N = p->N, M = p->M;
+    int* cnt = nullptr;
+    SPTB_CUDA(cudaMalloc(&cnt, sizeof(int) * (N + 1)));
+    SPTB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (N + 1), st));
+    k_count<<<grid_of(N), 256, 0, st>>>(a, cnt);
+    SPTB_LAUNCHED();
+
+    DevCSR& SH = p->SH;
+    SH.rows = N;
+    SH.cols = M;
+    SPTB_CUDA(cudaMalloc(&SH.row_ptr, sizeof(int) * (N + 1)));
+    size_t tmp_bytes = 0;
+    SPTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, SH.row_ptr, (int)(N + 1), st));
+    void* tmp = nullptr;
+    SPTB_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    SPTB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, SH.row_ptr, (int)(N + 1), st));
+    SPTB_CUDA(cudaFree(tmp));
+    int nnz = 0;
+    SPTB_CUDA(cudaMemcpyAsync(&nnz, SH.row_ptr + N, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SPTB_CUDA(cudaStreamSynchronize(st));
+    SH.nnz = nnz;
+    SH.max_row = a.W * a.W;
+
+    const size_t nn = nnz > 0 ? (size_t)nnz : 1;
+    int* ent_s = nullptr;
+    SPTB_CUDA(cudaMalloc(&SH.col, sizeof(int) * nn));
+    SPTB_CUDA(cudaMalloc(&SH.val, sizeof(C) * nn));
+    SPTB_CUDA(cudaMalloc(&ent_s, sizeof(int) * nn));
+    k_fill<C><<<grid_of(N), 256, 0, st>>>(a, SH.row_ptr, SH.col, (C*)SH.val, ent_s);
+    SPTB_LAUNCHED();
+
+    // S = (S^H)^H : stable radix sort of entries by grid row
+    DevCSR& S = p->S;
+    S.rows = M;
+    S.cols = N;
+    S.nnz = nnz;
+    SPTB_CUDA(cudaMalloc(&S.row_ptr, sizeof(int) * (M + 1)));
+    SPTB_CUDA(cudaMalloc(&S.col, sizeof(int) * nn));
+    SPTB_CUDA(cudaMalloc(&S.val, sizeof(C) * nn));
+    int *keys_out = nullptr, *idx_in = nullptr, *idx_out = nullptr, *rcnt = nullptr;
+    SPTB_CUDA(cudaMalloc(&keys_out, sizeof(int) * nn));
+    SPTB_CUDA(cudaMalloc(&idx_in, sizeof(int) * nn));
+    SPTB_CUDA(cudaMalloc(&idx_out, sizeof(int) * nn));
+    SPTB_CUDA(cudaMalloc(&rcnt, sizeof(int) * (M + 1)));
+    k_iota<<<grid_of(nnz), 256, 0, st>>>(idx_in, nnz);
+    SPTB_LAUNCHED();
+    int end_bit = 1;
+    while ((1LL << end_bit) < M) ++end_bit;
+    tmp_bytes = 0;
+    SPTB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, SH.col, keys_out, idx_in,
+                                              idx_out, nnz, 0, end_bit, st));
+    SPTB_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    SPTB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, SH.col, keys_out, idx_in, idx_out,
+                                              nnz, 0, end_bit, st));
+    SPTB_CUDA(cudaFree(tmp));
+    SPTB_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int) * (M + 1), st));
+    k_row_hist<<<grid_of(nnz), 256, 0, st>>>(keys_out, nnz, rcnt);
+    SPTB_LAUNCHED();
+    tmp_bytes = 0;
+    SPTB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, rcnt, S.row_ptr, (int)(M + 1), st));
+    SPTB_CUDA(cudaMalloc(&tmp, tmp_bytes));
+    SPTB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, rcnt, S.row_ptr, (int)(M + 1), st));
+    int* dmax = nullptr;
+    SPTB_CUDA(cudaMalloc(&dmax, sizeof(int)));
+    size_t tb2 = 0;
+    SPTB_CUDA(cub::DeviceReduce::Max(nullptr, tb2, rcnt, dmax, (int)M, st));
+    void* tmp2 = nullptr;
+    SPTB_CUDA(cudaMalloc(&tmp2, tb2));
+    SPTB_CUDA(cub::DeviceReduce::Max(tmp2, tb2, rcnt, dmax, (int)M, st));
+    k_gather_S<C><<<grid_of(nnz), 256, 0, st>>>(idx_out, ent_s, (const C*)SH.val, S.col,
+                                                 (C*)S.val, nnz);
+    SPTB_LAUNCHED();
+    int mx = 0;
+    SPTB_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SPTB_CUDA(cudaStreamSynchronize(st));
+    S.max_row = mx;
+    for (void* q : {(void*)tmp, tmp2, (void*)dmax, (void*)keys_out, (void*)idx_in,
+                    (void*)idx_out, (void*)rcnt, (void*)ent_s, (void*)cnt})
+        SPTB_CUDA(cudaFree(q));
+    return SPTB_OK;
+}
+
+// ---------------------------------------------------------------- host math
+
+double bessel_i0(double x) {
+    // power series sum_k ((x/2)^k / k!)^2, converges for all x
+    const double q = 0.25 * x * x;
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 1000; ++k) {
+        term *= q / ((double)k * (double)k);
+        sum += term;
+        if (term < 1e-18 * sum) break;
+    }
+    return sum;
+}
+
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        double z = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+        double dp = 0;
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = 0.0;
+            for (int k = 1; k <= n; ++k) {
+                const double p2 = p1;
+                p1 = p0;
+                p0 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p2) / k;
+            }
+            dp = n * (z * p0 - p1) / (z * z - 1.0);
+            const double dz = p0 / dp;
+            z -= dz;
+            if (std::fabs(dz) < 1e-16) break;
+        }
+        x[i] = -z;
+        w[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
+// kernel_transform (geometry.py:164-191)
+double kernel_ft(const sptb_kernel& k, double nu) {
+    if (k.family == SPTB_KERNEL_KB) {
+        const double w = k.width;
+        const double z2 = k.beta * k.beta - (M_PI * w * nu) * (M_PI * w * nu);
+        double out;
+        if (z2 > 0) {
+            const double z = std::sqrt(z2);
+            out = std::sinh(z) / z;
+        } else {
+            const double z = std::sqrt(-z2);
+            out = (std::fabs(z) < 1e-12) ? 1.0 : std::sin(z) / z;
+        }
+        return out * (w / bessel_i0(k.beta));
+    }
+    static thread_local std::vector<double> gx, gw;
+    if (gx.size() != 64) gauss_legendre(64, gx, gw);
+    const double half = k.width / 2.0;
+    double s = 0;
+    for (int i = 0; i < 64; ++i) {
+        const double t = gx[i] * half;
+        s += std::cos(2.0 * M_PI * nu * t) * std::exp(-0.5 * (t / k.sigma) * (t / k.sigma)) *
+             gw[i] * half;
+    }
+    return s;
+}
+
+}  // namespace
+
+int build_deapo(sptb_plan* p, const sptb_kernel* k) {
+    const int X = p->X, Y = p->Y;
+    std::vector<double> ax(X), ay(Y);
+    for (int i = 0; i < X; ++i) ax[i] = kernel_ft(*k, (i - X / 2.0) / X);
+    for (int i = 0; i < Y; ++i) ay[i] = kernel_ft(*k, (i - Y / 2.0) / Y);
+    double mx = 0;
+    for (double a : ay)
+        for (double b : ax) mx = std::max(mx, std::fabs(a * b));
+    const double eps = 1e-6 * mx;
+    const double r = std::min(X, Y) / 2.0;
+    p->deapo_host.assign((size_t)X * Y, 0.0);
+    long long bad = 0;
+    for (int y = 0; y < Y; ++y) {
+        const double dy = y - Y / 2.0;
+        for (int x = 0; x < X; ++x) {
+            const double dx = x - X / 2.0;
+            if (!(dy * dy + dx * dx < r * r)) continue;
+            const double apod = ay[y] * ax[x];
+            if (std::fabs(apod) < eps) {
+                ++bad;
+                continue;
+            }
+            const long long sgn = ((x - X / 2) + (y - Y / 2)) % 2;
+            p->deapo_host[(size_t)y * X + x] = (sgn == 0 ? 1.0 : -1.0) / apod;
+        }
+    }
+    if (bad)
+        return fail(SPTB_ERR_NEAR_ZERO, "kernel transform vanishes at " + std::to_string(bad) +
+                                            " supported grid points; narrow the kernel");
+    const size_t n = (size_t)X * Y;
+    if (p->prec == SPTB_PREC_F64) {
+        SPTB_CUDA(cudaMalloc(&p->deapo, n * sizeof(double)));
+        SPTB_CUDA(cudaMemcpy(p->deapo, p->deapo_host.data(), n * sizeof(double),
+                             cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(n);
+        for (size_t i = 0; i < n; ++i) f[i] = (float)p->deapo_host[i];
+        SPTB_CUDA(cudaMalloc(&p->deapo, n * sizeof(float)));
+        SPTB_CUDA(cudaMemcpy(p->deapo, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    return SPTB_OK;
+}
+
+int build_matrices(sptb_plan* p, const sptb_geometry* g, const sptb_kernel* k) {
+    const int P = p->P, T = p->T;
+    std::vector<double2> ramp(P);
+    std::vector<char> neg(P, 0);
+    const int h = P / 2;
+    for (int j = 0; j < P; ++j) {
+        const double pj = (double)(((j + h) % P) - h);
+        neg[j] = pj < 0 && !((P % 2 == 0) && j == P / 2);
+        const double th = ((2.0 * M_PI) * p->center) * pj / P;
+        ramp[j] = make_double2(std::cos(th), std::sin(th));
+    }
+    for (int j = 0; j < P; ++j)
+        if (neg[j]) {
+            const double2 m = ramp[(P - j) % P];
+            ramp[j] = make_double2(m.x, -m.y);  // gridding.py:130-131
+        }
+    double *dct = nullptr, *dst = nullptr;
+    double2* dramp = nullptr;
+    SPTB_CUDA(cudaMalloc(&dct, sizeof(double) * T));
+    SPTB_CUDA(cudaMalloc(&dst, sizeof(double) * T));
+    SPTB_CUDA(cudaMalloc(&dramp, sizeof(double2) * P));
+    SPTB_CUDA(cudaMemcpy(dct, g->cos_theta, sizeof(double) * T, cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMemcpy(dst, g->sin_theta, sizeof(double) * T, cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMemcpy(dramp, ramp.data(), sizeof(double2) * P, cudaMemcpyHostToDevice));
+    BuildArgs a;
+    a.P = P;
+    a.T = T;
+    a.X = p->X;
+    a.Y = p->Y;
+    a.W = k->width;
+    a.family = k->family;
+    a.beta = k->beta;
+    a.sigma = k->sigma;
+    a.i0beta = bessel_i0(k->beta);
+    a.thr = p->threshold;
+    a.ct = dct;
+    a.st = dst;
+    a.ramp = dramp;
+    int rc = (p->prec == SPTB_PREC_F64) ? build_typed<double2>(p, a) : build_typed<float2>(p, a);
+    cudaFree(dct);
+    cudaFree(dst);
+    cudaFree(dramp);
+    if (rc != SPTB_OK) return rc;
+    return build_deapo(p, k);
+}
+
+// ---------------------------------------------------------------- filter fold
+
+template <typename C, typename R>
+__global__ void k_fold(const int* col, const C* v, C* out, const R* w, long long wlen,
+                       long long N, int P, long long nnz) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nnz;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long s = col[i];
+        const R f = (wlen == N) ? w[s] : w[s % P];
+        C c = v[i];
+        c.x *= f;
+        c.y *= f;
+        out[i] = c;
+    }
+}
+
+// w_host -> w_dev (plan precision)
+int upload_weights(sptb_plan* p) {
+    if (p->w_dev) {
+        cudaFree(p->w_dev);
+        p->w_dev = nullptr;
+    }
+    p->w_len = (int64_t)p->w_host.size();
+    if (p->w_len == 0) return SPTB_OK;
+    const size_t rs = p->csize / 2;
+    SPTB_CUDA(cudaMalloc(&p->w_dev, rs * p->w_len));
+    if (p->prec == SPTB_PREC_F64) {
+        SPTB_CUDA(cudaMemcpy(p->w_dev, p->w_host.data(), rs * p->w_len, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(p->w_len);
+        for (int64_t i = 0; i < p->w_len; ++i) f[i] = (float)p->w_host[i];
+        SPTB_CUDA(cudaMemcpy(p->w_dev, f.data(), rs * p->w_len, cudaMemcpyHostToDevice));
+    }
+    return SPTB_OK;
+}
+
+int fold_filter(sptb_plan* p) {
+    const long long nnz = p->S.nnz;
+    const size_t cs = p->csize;
+    if (p->SW_val) {
+        cudaFree(p->SW_val);
+        p->SW_val = nullptr;
+    }
+    SPTB_TRY(upload_weights(p));
+    if (p->w_len == 0) return SPTB_OK;
+    SPTB_CUDA(cudaMalloc(&p->SW_val, cs * (nnz > 0 ? nnz : 1)));
+    if (nnz == 0) return SPTB_OK;
+    // weights multiply in double like the reference's folded build (gridding.py:146-152)
+    // -- float plans round the folded value once.
+    if (p->prec == SPTB_PREC_F64)
+        k_fold<double2, double><<<grid_of(nnz), 256, 0, p->stream>>>(
+            p->S.col, (const double2*)p->S.val, (double2*)p->SW_val, (const double*)p->w_dev,
+            p->w_len, p->N, p->P, nnz);
+    else
+        k_fold<float2, float><<<grid_of(nnz), 256, 0, p->stream>>>(
+            p->S.col, (const float2*)p->S.val, (float2*)p->SW_val, (const float*)p->w_dev,
+            p->w_len, p->N, p->P, nnz);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+}  // namespace sptb

@@ -1,0 +1,162 @@
+// Internal declarations shared by the sptb translation units.
+//
+// Device data layout (per plan, B = complex vectors in one launch):
+//   grid vectors, real space   : [b][y][x]   ("G" buffers, cuFFT 2D native)
+//   grid vectors, SpMM operand : [m][b]      m = y*n_x + x (batch innermost)
+//   sino vectors, real space   : [b][t][p]   ("S" buffers, cuFFT 1D native)
+//   sino vectors, SpMM side    : [s][b]      s = t*n_p + p
+// The batch-innermost layouts give every gathered nonzero a contiguous
+// B*sizeof(complex) run (128-bit lane loads); the batch-outer layouts keep
+// cuFFT on its fast contiguous path (measured: batch-inner 2D cuFFT is 11x
+// slower on B200, profiles/r01_fftprobe.txt).  Transposes between the two are
+// fused into SpMM epilogues where the SpMM writes, and are standalone tiled
+// transposes where it reads.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/sptb.h"
+
+namespace sptb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+void count_launch(int n = 1);
+
+#define SPTB_CUDA(expr)                                                     \
+    do {                                                                    \
+        cudaError_t _e = (expr);                                            \
+        if (_e != cudaSuccess)                                              \
+            return ::sptb::fail(SPTB_ERR_CUDA, std::string(#expr) + ": " +  \
+                                cudaGetErrorString(_e));                    \
+    } while (0)
+
+#define SPTB_CUFFT(expr)                                                    \
+    do {                                                                    \
+        cufftResult _r = (expr);                                            \
+        if (_r != CUFFT_SUCCESS)                                            \
+            return ::sptb::fail(SPTB_ERR_CUFFT, std::string(#expr) +        \
+                                " -> cufftResult " + std::to_string((int)_r)); \
+    } while (0)
+
+#define SPTB_TRY(expr)                                                      \
+    do {                                                                    \
+        int _s = (expr);                                                    \
+        if (_s != SPTB_OK) return _s;                                       \
+    } while (0)
+
+#define SPTB_LAUNCHED()                                                     \
+    do {                                                                    \
+        ::sptb::count_launch();                                             \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess)                                              \
+            return ::sptb::fail(SPTB_ERR_CUDA, std::string("launch: ") +    \
+                                cudaGetErrorString(_e));                    \
+    } while (0)
+
+// CSR matrix on the device (int32 indices, complex values of plan precision)
+struct DevCSR {
+    int64_t rows = 0, cols = 0, nnz = 0;
+    int* row_ptr = nullptr;   // rows + 1
+    int* col = nullptr;       // nnz
+    void* val = nullptr;      // nnz complex (float2 or double2)
+    int max_row = 0;          // longest row
+};
+
+struct FFTPlans {
+    cufftHandle fft2 = 0;   // Y x X, batch B, [b][y][x]
+    cufftHandle fft1 = 0;   // n_p,   batch B*T, [b][t][p]
+};
+
+}  // namespace sptb
+
+struct sptb_plan {
+    int device = 0;
+    int prec = SPTB_PREC_F32;
+    int P = 0, T = 0, X = 0, Y = 0;
+    int64_t M = 0, N = 0;
+    double center = 0;
+    int max_batch = 1;
+    double threshold = 0;
+    cudaStream_t stream = nullptr;
+    size_t csize = 8;          // bytes per complex element
+
+    sptb::DevCSR S, SH;        // S: M x N rows=grid, SH: N x M rows=samples
+    void* SW_val = nullptr;    // S values with the filter folded (nullptr: none)
+    std::vector<double> w_host;  // filter weights (n_p or N), empty = none
+    void* w_dev = nullptr;       // real weights of plan precision (n_p or N)
+    int64_t w_len = 0;
+    double calib = 1.0;
+
+    void* deapo = nullptr;     // M real (plan precision), row-major [y][x]
+    std::vector<double> deapo_host;
+
+    // work buffers (max_batch complex vectors each)
+    void* G0 = nullptr;  // grid [b][m]  (FFT2 in place)
+    void* G1 = nullptr;  // grid [m][b]
+    void* G2 = nullptr;  // extra grid buffers for solvers
+    void* S0 = nullptr;  // sino [b][s]  (FFT1 in place)
+    void* S1 = nullptr;  // sino [s][b]
+    int work_B = 0;      // batch the work buffers are sized for
+    // caller-format staging for host pointers
+    void* stage_in = nullptr;
+    size_t stage_in_bytes = 0;
+    void* stage_out = nullptr;
+    size_t stage_out_bytes = 0;
+    // reduction scratch
+    double* red = nullptr;
+    size_t red_len = 0;
+
+    std::map<int, sptb::FFTPlans> ffts;  // keyed by batch
+    void* fft_work = nullptr;
+    size_t fft_work_bytes = 0;
+
+    std::vector<void*> extra;            // solver-owned device buffers
+};
+
+namespace sptb {
+
+// ---------------------------------------------------------------- helpers
+int get_fft(sptb_plan* p, int B, FFTPlans** out);
+int ensure_work(sptb_plan* p, int B);
+int ensure_stage(void** buf, size_t* have, size_t need);
+int is_device_ptr(const void* ptr, bool* dev);
+
+// ---------------------------------------------------------------- matrix build
+int build_matrices(sptb_plan* p, const sptb_geometry* g, const sptb_kernel* k);
+int fold_filter(sptb_plan* p);
+int upload_weights(sptb_plan* p);
+
+// ---------------------------------------------------------------- kernels (templated on precision)
+// SpMM  y = A x, x: [col][B]; trans_out: y written [b][row] (else [row][b]);
+// sub != nullptr: y = sub - A x  ([row][b], non-transposed only)
+template <typename R>
+int launch_spmm(const DevCSR& A, const void* val, const void* x, void* y, int B,
+                bool trans_out, const void* sub, cudaStream_t st);
+
+template <typename R>
+int launch_transpose_bm_to_mb(const void* in, void* out, int B, int64_t M, cudaStream_t st);
+
+// pack caller slices -> complex [b][len] (optionally times a real plane)
+// unpack complex [b][len] -> caller slices, times plane (optional) * scale
+template <typename R>
+int launch_pack(const void* in, int fmt, int64_t n, int64_t u0, int nb, int B,
+                int64_t len, const void* plane, void* out, cudaStream_t st);
+template <typename R>
+int launch_unpack(const void* in, int64_t len, const void* plane, double scale,
+                  void* out, int fmt, int64_t n, int64_t u0, int nb, cudaStream_t st);
+// multiply [b][t][p] by real weights indexed p (len P) or s (len T*P)
+template <typename R>
+int launch_weight_sino(void* z, const void* w, int64_t wlen, int P, int64_t N, int B,
+                       cudaStream_t st);
+template <typename R>
+int launch_permute_grid(const void* in, void* out, int X, int Y, int B, bool f_to_c,
+                        cudaStream_t st);
+
+}  // namespace sptb

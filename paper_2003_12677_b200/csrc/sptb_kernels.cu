@@ -1,0 +1,479 @@
+// Hot-path kernels: gridding SpMM (K1/K2), layout transposes, pack/unpack
+// (K3-K6 elementwise stages).  sm_100a, no tensor cores: every kernel here is
+// HBM/L2-bound.
+#include "sptb_internal.cuh"
+
+#include <algorithm>
+
+namespace sptb {
+
+template <typename R> struct Cplx;
+template <> struct Cplx<float> { using T = float2; };
+template <> struct Cplx<double> { using T = double2; };
+
+// 8- or 16-byte lane chunk holding CW complex values
+template <typename R, int CW> struct Chunk;
+template <> struct Chunk<float, 1> {
+    using T = float2;
+    static __device__ __forceinline__ void ld(const void* p, float2 (&c)[1]) {
+        c[0] = __ldg(reinterpret_cast<const float2*>(p));
+    }
+};
+template <> struct Chunk<float, 2> {
+    using T = float4;
+    static __device__ __forceinline__ void ld(const void* p, float2 (&c)[2]) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        c[0] = make_float2(v.x, v.y);
+        c[1] = make_float2(v.z, v.w);
+    }
+};
+template <> struct Chunk<double, 1> {
+    using T = double2;
+    static __device__ __forceinline__ void ld(const void* p, double2 (&c)[1]) {
+        c[0] = __ldg(reinterpret_cast<const double2*>(p));
+    }
+};
+
+template <typename C>
+__device__ __forceinline__ void cmac(C& acc, const C& a, const C& b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMM over a batch-innermost dense operand.
+//
+// One CTA owns TILE consecutive rows.  A "group" of G lanes computes one row
+// for all BB = G*CPL*CW batch columns (every gathered nonzero is one
+// contiguous BB*sizeof(C) run of x -> 8/16-byte coalesced lane loads).
+// Rows longer than LMAX nonzeros (the skewed centre of S: up to 4852 at
+// 2048^2 x 1536) are split into NCH fixed chunks shared by all groups of the
+// CTA and combined in chunk order, so results are deterministic and do not
+// depend on which group ran which chunk.
+// TRANS: the tile is staged in shared memory and written [b][row] (the
+// batch-outer layout cuFFT wants), i.e. the layout transpose is fused into
+// the epilogue.  SUB: y = sub - A x  ([row][b]).
+// ---------------------------------------------------------------------------
+constexpr int SPMM_THREADS = 256;
+constexpr int LMAX = 64;
+constexpr int NCH = 16;
+constexpr int UNR = 8;
+
+template <typename R, int G, int CPL, int CW>
+struct SpmmCfg {
+    static constexpr int BB = G * CPL * CW;
+    static constexpr int NG = SPMM_THREADS / G;
+    static constexpr int TILE = (4 * NG < 32) ? 32 : 4 * NG;
+};
+
+template <typename R, int G, int CPL, int CW>
+__device__ __forceinline__ void row_accumulate(
+    const int* __restrict__ ci, const typename Cplx<R>::T* __restrict__ cv,
+    const typename Cplx<R>::T* __restrict__ x, int beg, int end, int lig,
+    typename Cplx<R>::T (&acc)[CPL][CW]) {
+    using C = typename Cplx<R>::T;
+    constexpr int BB = G * CPL * CW;
+    for (int k = beg; k < end; k += UNR) {
+        int cc[UNR];
+        C vv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int kk = k + u;
+            const bool ok = kk < end;
+            cc[u] = ok ? __ldg(ci + kk) : 0;
+            C z;
+            z.x = 0;
+            z.y = 0;
+            vv[u] = ok ? cv[kk] : z;
+        }
+        C xs[UNR][CPL][CW];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+                if (k + u < end) {
+                    const C* src = x + (size_t)cc[u] * BB + (size_t)(q * G + lig) * CW;
+                    Chunk<R, CW>::ld(src, xs[u][q]);
+                } else {
+#pragma unroll
+                    for (int w = 0; w < CW; ++w) {
+                        xs[u][q][w].x = 0;
+                        xs[u][q][w].y = 0;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int w = 0; w < CW; ++w) cmac(acc[q][w], vv[u], xs[u][q][w]);
+    }
+}
+
+template <typename R, int G, int CPL, int CW, bool TRANS, bool SUB>
+__global__ void __launch_bounds__(SPMM_THREADS)
+k_spmm(const int* __restrict__ rp, const int* __restrict__ ci,
+       const typename Cplx<R>::T* __restrict__ cv,
+       const typename Cplx<R>::T* __restrict__ x, typename Cplx<R>::T* __restrict__ y,
+       const typename Cplx<R>::T* __restrict__ sub, int rows) {
+    using C = typename Cplx<R>::T;
+    using Cfg = SpmmCfg<R, G, CPL, CW>;
+    constexpr int BB = Cfg::BB, NG = Cfg::NG, TILE = Cfg::TILE;
+    constexpr int LD = BB + 1;  // padded smem row (bank spread)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* part = reinterpret_cast<C*>(smem_raw);  // [NCH][BB]
+    C* tile = part + NCH * BB;                 // [TILE][LD] (TRANS only)
+    __shared__ int s_rp[TILE + 1];
+
+    const int tid = threadIdx.x;
+    const int g = tid / G, lig = tid % G;
+    const int row0 = blockIdx.x * TILE;
+    const int nrows = min(TILE, rows - row0);
+    for (int i = tid; i <= nrows; i += SPMM_THREADS) s_rp[i] = rp[row0 + i];
+    __syncthreads();
+
+    auto emit = [&](int r, const C (&a)[CPL][CW]) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int w = 0; w < CW; ++w) {
+                const int b = (q * G + lig) * CW + w;
+                if (TRANS) {
+                    tile[r * LD + b] = a[q][w];
+                } else {
+                    const size_t o = (size_t)(row0 + r) * BB + b;
+                    C v = a[q][w];
+                    if (SUB) {
+                        C s = sub[o];
+                        v.x = s.x - v.x;
+                        v.y = s.y - v.y;
+                    }
+                    y[o] = v;
+                }
+            }
+    };
+
+    // short rows: one group per row
+    for (int r = g; r < nrows; r += NG) {
+        const int beg = s_rp[r], end = s_rp[r + 1];
+        if (end - beg > LMAX) continue;
+        C acc[CPL][CW];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int w = 0; w < CW; ++w) {
+                acc[q][w].x = 0;
+                acc[q][w].y = 0;
+            }
+        row_accumulate<R, G, CPL, CW>(ci, cv, x, beg, end, lig, acc);
+        emit(r, acc);
+    }
+
+    // long rows: NCH fixed chunks over all groups, combined in chunk order
+    for (int r = 0; r < nrows; ++r) {
+        const int beg = s_rp[r], end = s_rp[r + 1];
+        const int len = end - beg;
+        if (len <= LMAX) continue;
+        for (int c = g; c < NCH; c += NG) {
+            const int cb = beg + (int)(((long long)len * c) / NCH);
+            const int ce = beg + (int)(((long long)len * (c + 1)) / NCH);
+            C acc[CPL][CW];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int w = 0; w < CW; ++w) {
+                    acc[q][w].x = 0;
+                    acc[q][w].y = 0;
+                }
+            row_accumulate<R, G, CPL, CW>(ci, cv, x, cb, ce, lig, acc);
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int w = 0; w < CW; ++w) part[c * BB + (q * G + lig) * CW + w] = acc[q][w];
+        }
+        __syncthreads();
+        for (int b = tid; b < BB; b += SPMM_THREADS) {
+            C s = part[b];
+            for (int c = 1; c < NCH; ++c) {
+                s.x += part[c * BB + b].x;
+                s.y += part[c * BB + b].y;
+            }
+            if (TRANS) {
+                tile[r * LD + b] = s;
+            } else {
+                const size_t o = (size_t)(row0 + r) * BB + b;
+                if (SUB) {
+                    C t = sub[o];
+                    s.x = t.x - s.x;
+                    s.y = t.y - s.y;
+                }
+                y[o] = s;
+            }
+        }
+        __syncthreads();
+    }
+
+    if (TRANS) {
+        __syncthreads();
+        // y[b][row0 + i]: consecutive threads -> consecutive rows
+        for (int e = tid; e < BB * TILE; e += SPMM_THREADS) {
+            const int b = e / TILE, i = e % TILE;
+            if (i < nrows) y[(size_t)b * rows + row0 + i] = tile[i * LD + b];
+        }
+    }
+}
+
+template <typename R, int G, int CPL, int CW>
+static int spmm_dispatch(const DevCSR& A, const void* val, const void* x, void* y,
+                         bool trans, const void* sub, cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    using Cfg = SpmmCfg<R, G, CPL, CW>;
+    const int rows = (int)A.rows;
+    if (rows == 0) return SPTB_OK;
+    const int grid = (rows + Cfg::TILE - 1) / Cfg::TILE;
+    size_t sm = (size_t)NCH * Cfg::BB * sizeof(C);
+    if (trans) sm += (size_t)Cfg::TILE * (Cfg::BB + 1) * sizeof(C);
+    auto run = [&](auto kern) -> int {
+        if (sm > 48 * 1024) SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<grid, SPMM_THREADS, sm, st>>>(A.row_ptr, A.col, (const C*)val, (const C*)x,
+                                             (C*)y, (const C*)sub, rows);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    };
+    if (trans) return run(k_spmm<R, G, CPL, CW, true, false>);
+    if (sub) return run(k_spmm<R, G, CPL, CW, false, true>);
+    return run(k_spmm<R, G, CPL, CW, false, false>);
+}
+
+template <>
+int launch_spmm<float>(const DevCSR& A, const void* val, const void* x, void* y, int B,
+                       bool trans, const void* sub, cudaStream_t st) {
+    if (trans && sub) return fail(SPTB_ERR_ARG, "spmm: trans+sub unsupported");
+    switch (B) {
+        case 1: return spmm_dispatch<float, 1, 1, 1>(A, val, x, y, trans, sub, st);
+        case 2: return spmm_dispatch<float, 1, 1, 2>(A, val, x, y, trans, sub, st);
+        case 4: return spmm_dispatch<float, 2, 1, 2>(A, val, x, y, trans, sub, st);
+        case 8: return spmm_dispatch<float, 4, 1, 2>(A, val, x, y, trans, sub, st);
+        case 16: return spmm_dispatch<float, 8, 1, 2>(A, val, x, y, trans, sub, st);
+        case 32: return spmm_dispatch<float, 16, 1, 2>(A, val, x, y, trans, sub, st);
+        case 64: return spmm_dispatch<float, 32, 1, 2>(A, val, x, y, trans, sub, st);
+    }
+    return fail(SPTB_ERR_ARG, "spmm: batch must be a power of two <= 64");
+}
+
+template <>
+int launch_spmm<double>(const DevCSR& A, const void* val, const void* x, void* y, int B,
+                        bool trans, const void* sub, cudaStream_t st) {
+    if (trans && sub) return fail(SPTB_ERR_ARG, "spmm: trans+sub unsupported");
+    switch (B) {
+        case 1: return spmm_dispatch<double, 1, 1, 1>(A, val, x, y, trans, sub, st);
+        case 2: return spmm_dispatch<double, 2, 1, 1>(A, val, x, y, trans, sub, st);
+        case 4: return spmm_dispatch<double, 4, 1, 1>(A, val, x, y, trans, sub, st);
+        case 8: return spmm_dispatch<double, 8, 1, 1>(A, val, x, y, trans, sub, st);
+        case 16: return spmm_dispatch<double, 16, 1, 1>(A, val, x, y, trans, sub, st);
+        case 32: return spmm_dispatch<double, 32, 1, 1>(A, val, x, y, trans, sub, st);
+        case 64: return spmm_dispatch<double, 32, 2, 1>(A, val, x, y, trans, sub, st);
+    }
+    return fail(SPTB_ERR_ARG, "spmm: batch must be a power of two <= 64");
+}
+
+// ---------------------------------------------------------------------------
+// [b][m] -> [m][b] tiled transpose (B <= 64): 32 m x B tile through smem.
+// ---------------------------------------------------------------------------
+template <typename C>
+__global__ void __launch_bounds__(256) k_transpose_bm_mb(const C* __restrict__ in,
+                                                         C* __restrict__ out, int B,
+                                                         long long M) {
+    __shared__ C t[64][33];
+    const long long m0 = (long long)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int b = ty; b < B; b += 8) {
+        const long long m = m0 + tx;
+        if (m < M) t[b][tx] = in[(size_t)b * M + m];
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const long long m = m0 + i;
+        if (m >= M) break;
+        for (int b = tx; b < B; b += 32) out[(size_t)m * B + b] = t[b][i];
+    }
+}
+
+template <typename R>
+int launch_transpose_bm_to_mb(const void* in, void* out, int B, int64_t M, cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    if (B > 64) return fail(SPTB_ERR_ARG, "transpose: B > 64");
+    const int grid = (int)((M + 31) / 32);
+    k_transpose_bm_mb<C><<<grid, 256, 0, st>>>((const C*)in, (C*)out, B, M);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template int launch_transpose_bm_to_mb<float>(const void*, void*, int, int64_t, cudaStream_t);
+template int launch_transpose_bm_to_mb<double>(const void*, void*, int, int64_t, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// pack / unpack between caller slices and complex [b][len]
+// (pairing a + ib of slices (2k, 2k+1): pipeline.py:122-159)
+// ---------------------------------------------------------------------------
+template <typename TI, typename R>
+__global__ void k_pack(const TI* __restrict__ in, bool cplx, long long n, long long u0, int nb,
+                       long long len, const R* __restrict__ plane,
+                       typename Cplx<R>::T* __restrict__ out, int B) {
+    using C = typename Cplx<R>::T;
+    const long long total = (long long)B * len;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(e / len);
+        const long long i = e - (long long)b * len;
+        C v;
+        v.x = 0;
+        v.y = 0;
+        if (b < nb) {
+            const long long u = u0 + b;
+            R re, im;
+            if (cplx) {
+                re = (R)in[(u * len + i) * 2];
+                im = (R)in[(u * len + i) * 2 + 1];
+            } else {
+                re = (R)in[(2 * u) * len + i];
+                im = (2 * u + 1 < n) ? (R)in[(2 * u + 1) * len + i] : (R)0;
+            }
+            if (plane) {
+                const R d = plane[i];
+                re *= d;
+                im *= d;
+            }
+            v.x = re;
+            v.y = im;
+        }
+        out[e] = v;
+    }
+}
+
+template <typename TO, typename R>
+__global__ void k_unpack(const typename Cplx<R>::T* __restrict__ z, long long len,
+                         const R* __restrict__ plane, R scale, TO* __restrict__ out, bool cplx,
+                         long long n, long long u0, int nb) {
+    const long long total = (long long)nb * len;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(e / len);
+        const long long i = e - (long long)b * len;
+        const long long u = u0 + b;
+        R f = scale;
+        if (plane) f *= plane[i];
+        const auto v = z[e];
+        const R re = v.x * f, im = v.y * f;
+        if (cplx) {
+            out[(u * len + i) * 2] = (TO)re;
+            out[(u * len + i) * 2 + 1] = (TO)im;
+        } else {
+            out[(2 * u) * len + i] = (TO)re;
+            if (2 * u + 1 < n) out[(2 * u + 1) * len + i] = (TO)im;
+        }
+    }
+}
+
+static int grid_for(long long total) {
+    long long g = (total + 255) / 256;
+    return (int)std::min<long long>(g, 148LL * 32);
+}
+
+template <typename R>
+int launch_pack(const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, int64_t len,
+                const void* plane, void* out, cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    const bool cplx = fmt & SPTB_FMT_COMPLEX;
+    const int grid = grid_for((long long)B * len);
+    if (fmt & SPTB_FMT_F64)
+        k_pack<double, R><<<grid, 256, 0, st>>>((const double*)in, cplx, n, u0, nb, len,
+                                                (const R*)plane, (C*)out, B);
+    else
+        k_pack<float, R><<<grid, 256, 0, st>>>((const float*)in, cplx, n, u0, nb, len,
+                                               (const R*)plane, (C*)out, B);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template int launch_pack<float>(const void*, int, int64_t, int64_t, int, int, int64_t, const void*, void*, cudaStream_t);
+template int launch_pack<double>(const void*, int, int64_t, int64_t, int, int, int64_t, const void*, void*, cudaStream_t);
+
+template <typename R>
+int launch_unpack(const void* in, int64_t len, const void* plane, double scale, void* out,
+                  int fmt, int64_t n, int64_t u0, int nb, cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    const bool cplx = fmt & SPTB_FMT_COMPLEX;
+    const int grid = grid_for((long long)nb * len);
+    if (fmt & SPTB_FMT_F64)
+        k_unpack<double, R><<<grid, 256, 0, st>>>((const C*)in, len, (const R*)plane, (R)scale,
+                                                  (double*)out, cplx, n, u0, nb);
+    else
+        k_unpack<float, R><<<grid, 256, 0, st>>>((const C*)in, len, (const R*)plane, (R)scale,
+                                                 (float*)out, cplx, n, u0, nb);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template int launch_unpack<float>(const void*, int64_t, const void*, double, void*, int, int64_t, int64_t, int, cudaStream_t);
+template int launch_unpack<double>(const void*, int64_t, const void*, double, void*, int, int64_t, int64_t, int, cudaStream_t);
+
+// z[b][t][p] *= w[p] (wlen == P) or w[t*P+p] (wlen == N)
+template <typename R>
+__global__ void k_weight_sino(typename Cplx<R>::T* __restrict__ z, const R* __restrict__ w,
+                              long long wlen, int P, long long N, int B) {
+    const long long total = (long long)B * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long s = e % N;
+        const R f = (wlen == N) ? w[s] : w[s % P];
+        auto v = z[e];
+        v.x *= f;
+        v.y *= f;
+        z[e] = v;
+    }
+}
+
+template <typename R>
+int launch_weight_sino(void* z, const void* w, int64_t wlen, int P, int64_t N, int B,
+                       cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    k_weight_sino<R><<<grid_for((long long)B * N), 256, 0, st>>>((C*)z, (const R*)w, wlen, P, N, B);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template int launch_weight_sino<float>(void*, const void*, int64_t, int, int64_t, int, cudaStream_t);
+template int launch_weight_sino<double>(void*, const void*, int64_t, int, int64_t, int, cudaStream_t);
+
+// F-order grid rows (gx*Y+gy) <-> C-order rows (gy*X+gx), B complex per row
+template <typename C>
+__global__ void k_permute_grid(const C* __restrict__ in, C* __restrict__ out, int X, int Y,
+                               int B, bool f_to_c) {
+    const long long total = (long long)X * Y * B;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long mc = e / B;
+        const int b = (int)(e - mc * B);
+        const long long gy = mc / X, gx = mc - gy * X;
+        const long long mf = gx * Y + gy;
+        if (f_to_c)
+            out[e] = in[mf * B + b];
+        else
+            out[mf * B + b] = in[e];
+    }
+}
+
+template <typename R>
+int launch_permute_grid(const void* in, void* out, int X, int Y, int B, bool f_to_c,
+                        cudaStream_t st) {
+    using C = typename Cplx<R>::T;
+    k_permute_grid<C><<<grid_for((long long)X * Y * B), 256, 0, st>>>((const C*)in, (C*)out, X, Y,
+                                                                       B, f_to_c);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template int launch_permute_grid<float>(const void*, void*, int, int, int, bool, cudaStream_t);
+template int launch_permute_grid<double>(const void*, void*, int, int, int, bool, cudaStream_t);
+
+}  // namespace sptb

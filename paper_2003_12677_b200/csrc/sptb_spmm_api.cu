@@ -1,0 +1,133 @@
+// sptb_spmm: the reference's free spmv/spmm (operators.py:124-136) in the
+// reference's own index convention (F-order grid rows, nrhs innermost).
+#include "sptb_internal.cuh"
+
+#include <algorithm>
+
+namespace sptb {
+
+template <typename R> struct CplxT;
+template <> struct CplxT<float> { using T = float2; };
+template <> struct CplxT<double> { using T = double2; };
+
+// device row r  <-  caller row src(r); src = F-order index when permuting a grid
+__device__ __forceinline__ long long src_row(long long r, int X, int Y) {
+    if (X == 0) return r;
+    const long long gy = r / X, gx = r - gy * X;
+    return gx * Y + gy;
+}
+
+template <typename TI, typename R>
+__global__ void k_gather_cols(const TI* __restrict__ in, long long rows, long long nrhs,
+                              long long c0, int nb, int B, int X, int Y,
+                              typename CplxT<R>::T* __restrict__ out) {
+    const long long total = rows * B;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / B;
+        const int b = (int)(e - r * B);
+        typename CplxT<R>::T v;
+        v.x = 0;
+        v.y = 0;
+        if (b < nb) {
+            const long long o = (src_row(r, X, Y) * nrhs + c0 + b) * 2;
+            v.x = (R)in[o];
+            v.y = (R)in[o + 1];
+        }
+        out[e] = v;
+    }
+}
+
+template <typename TO, typename R>
+__global__ void k_scatter_cols(const typename CplxT<R>::T* __restrict__ in, long long rows,
+                               long long nrhs, long long c0, int nb, int B, int X, int Y,
+                               TO* __restrict__ out) {
+    const long long total = rows * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / nb;
+        const int b = (int)(e - r * nb);
+        const auto v = in[r * B + b];
+        const long long o = (src_row(r, X, Y) * nrhs + c0 + b) * 2;
+        out[o] = (TO)v.x;
+        out[o + 1] = (TO)v.y;
+    }
+}
+
+static int gridn(long long n) {
+    long long g = (n + 255) / 256;
+    return (int)std::min<long long>(std::max<long long>(g, 1), 148LL * 32);
+}
+
+template <typename R>
+int spmm_ref(sptb_plan* p, int which, const void* x, void* y, int64_t nrhs, int fmt) {
+    using C = typename CplxT<R>::T;
+    const DevCSR& A = (which == SPTB_MAT_SH) ? p->SH : p->S;
+    const void* vals = A.val;
+    if (which == SPTB_MAT_SW) {
+        if (!p->SW_val) return fail(SPTB_ERR_STATE, "no filter set");
+        vals = p->SW_val;
+    }
+    const bool grid_in = (which == SPTB_MAT_SH);
+    const int inX = grid_in ? p->X : 0, inY = grid_in ? p->Y : 0;
+    const int outX = grid_in ? 0 : p->X, outY = grid_in ? 0 : p->Y;
+    cudaStream_t st = p->stream;
+    const size_t eb = (fmt & SPTB_FMT_F64) ? 8 : 4;
+    bool dx = true, dy = true;
+    is_device_ptr(x, &dx);
+    is_device_ptr(y, &dy);
+    const void* xs = x;
+    void* ys = y;
+    const size_t xbytes = eb * 2 * (size_t)A.cols * nrhs, ybytes = eb * 2 * (size_t)A.rows * nrhs;
+    if (!dx) {
+        SPTB_TRY(ensure_stage(&p->stage_in, &p->stage_in_bytes, xbytes));
+        SPTB_CUDA(cudaMemcpyAsync(p->stage_in, x, xbytes, cudaMemcpyHostToDevice, st));
+        xs = p->stage_in;
+    }
+    if (!dy) {
+        SPTB_TRY(ensure_stage(&p->stage_out, &p->stage_out_bytes, ybytes));
+        ys = p->stage_out;
+    }
+    SPTB_TRY(ensure_work(p, [&] { int b = 1; while (b < std::min<int64_t>(p->max_batch, nrhs)) b <<= 1; return b; }()));
+    C* xin = (C*)(grid_in ? p->G1 : p->S1);
+    C* yout = (C*)(grid_in ? p->S0 : p->G0);
+    for (int64_t c0 = 0; c0 < nrhs; c0 += p->max_batch) {
+        const int nb = (int)std::min<int64_t>(p->max_batch, nrhs - c0);
+        int B = 1;
+        while (B < nb) B <<= 1;
+        if (fmt & SPTB_FMT_F64)
+            k_gather_cols<double, R><<<gridn(A.cols * B), 256, 0, st>>>(
+                (const double*)xs, A.cols, nrhs, c0, nb, B, inX, inY, xin);
+        else
+            k_gather_cols<float, R><<<gridn(A.cols * B), 256, 0, st>>>(
+                (const float*)xs, A.cols, nrhs, c0, nb, B, inX, inY, xin);
+        SPTB_LAUNCHED();
+        SPTB_TRY(launch_spmm<R>(A, vals, xin, yout, B, false, nullptr, st));
+        if (fmt & SPTB_FMT_F64)
+            k_scatter_cols<double, R><<<gridn(A.rows * nb), 256, 0, st>>>(
+                yout, A.rows, nrhs, c0, nb, B, outX, outY, (double*)ys);
+        else
+            k_scatter_cols<float, R><<<gridn(A.rows * nb), 256, 0, st>>>(
+                yout, A.rows, nrhs, c0, nb, B, outX, outY, (float*)ys);
+        SPTB_LAUNCHED();
+    }
+    if (!dy) SPTB_CUDA(cudaMemcpyAsync(y, ys, ybytes, cudaMemcpyDeviceToHost, st));
+    SPTB_CUDA(cudaStreamSynchronize(st));
+    return SPTB_OK;
+}
+
+}  // namespace sptb
+
+using namespace sptb;
+
+extern "C" int sptb_spmm(sptb_plan* p, int32_t which, const void* x, void* y, int64_t nrhs,
+                         int32_t fmt) {
+    if (!p) return fail(SPTB_ERR_ARG, "null plan");
+    if (!(fmt & SPTB_FMT_COMPLEX)) return fail(SPTB_ERR_ARG, "spmm operands are complex");
+    if (nrhs < 1) return fail(SPTB_ERR_ARG, "nrhs must be >= 1");
+    if (which != SPTB_MAT_S && which != SPTB_MAT_SH && which != SPTB_MAT_SW)
+        return fail(SPTB_ERR_ARG, "unknown matrix");
+    cudaSetDevice(p->device);
+    return p->prec == SPTB_PREC_F64 ? spmm_ref<double>(p, which, x, y, nrhs, fmt)
+                                    : spmm_ref<float>(p, which, x, y, nrhs, fmt);
+}

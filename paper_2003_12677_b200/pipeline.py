@@ -1,0 +1,303 @@
+"""Slice-parallel pipeline (API of sptomo/pipeline.py) over GPUs.
+
+The reference packs slices (2k, 2k+1) into one complex sinogram and farms
+pair units out to a fork pool (pipeline.py:137-235).  Here a unit is one
+complex vector of a device batch, and the "workers" are GPUs: one process per
+GPU under torch.distributed.  Rank 0 owns the stack; its pair-unit ranges are
+scattered to the ranks with NCCL point-to-point sends, every rank solves its
+range with the batched device solver (no collective inside iterations), and
+the reconstructed slices plus per-unit reports are gathered back to rank 0.
+Units never span ranks, so every slice's floating-point path is independent
+of the GPU count (same launch batch on every rank).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ShapeMismatchError, WorkerFailureError
+from .geometry import ScanGeometry
+
+PAIRING_TOL = 1e-5
+
+
+@dataclass(frozen=True)
+class SinogramStack:
+    """(n_z, n_theta, n_p) real stack plus geometry (pipeline.py:35-54)."""
+
+    data: np.ndarray
+    geometry: ScanGeometry
+
+    def __post_init__(self):
+        d = np.asarray(self.data, dtype=np.float64)
+        if d.ndim != 3:
+            raise ShapeMismatchError(f"sinogram stack must be 3D, got {d.shape}")
+        want = (self.geometry.n_z,) + tuple(self.geometry.sino_shape)
+        if d.shape != want:
+            raise ShapeMismatchError(f"sinogram stack shape {d.shape} != geometry {want}")
+        object.__setattr__(self, "data", d)
+
+    @property
+    def n_z(self) -> int:
+        return self.data.shape[0]
+
+
+@dataclass(frozen=True)
+class TomogramStack:
+    """(n_z, n_y, n_x) real stack (pipeline.py:57-71)."""
+
+    data: np.ndarray
+
+    def __post_init__(self):
+        d = np.asarray(self.data)
+        if d.ndim != 3:
+            raise ShapeMismatchError(f"tomogram stack must be 3D, got {d.shape}")
+        object.__setattr__(self, "data", d)
+
+    @property
+    def n_z(self) -> int:
+        return self.data.shape[0]
+
+
+@dataclass(frozen=True)
+class ChunkPlan:
+    """Passes x workers -> (start, length), in order (pipeline.py:74-94)."""
+
+    worker_count: int
+    max_slices_per_worker_pass: int
+    passes: tuple
+    halo: int = 0
+
+    @property
+    def n_passes(self) -> int:
+        return len(self.passes)
+
+    def nonempty_ranges(self):
+        return [r for row in self.passes for r in row if r[1] > 0]
+
+
+def plan_chunks(n_z: int, workers: int, max_per_pass: int = 8) -> ChunkPlan:
+    """ceil(n_z / (workers*max_per_pass)) passes; inside a pass lengths differ
+    by at most one and the short ones trail (pipeline.py:97-119)."""
+    for name, v, lo in (("n_z", n_z, 1), ("workers", workers, 1), ("max_per_pass", max_per_pass, 1)):
+        if v < lo:
+            raise ValueError(f"{name} must be >= {lo}, got {v}")
+    cap = workers * max_per_pass
+    rows, cursor = [], 0
+    for _ in range(math.ceil(n_z / cap)):
+        todo = min(cap, n_z - cursor)
+        q, r = divmod(todo, workers)
+        row = []
+        for w in range(workers):
+            ln = q + (w < r)
+            row.append((cursor, ln))
+            cursor += ln
+        rows.append(tuple(row))
+    return ChunkPlan(worker_count=workers, max_slices_per_worker_pass=max_per_pass,
+                     passes=tuple(rows))
+
+
+def pair_complex(a, b) -> np.ndarray:
+    """a + i b (pipeline.py:122-128)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ShapeMismatchError(f"pair shapes differ: {a.shape} vs {b.shape}")
+    return a + 1j * b
+
+
+def unpair(u):
+    """(Re u, Im u) as contiguous real arrays (pipeline.py:131-134)."""
+    u = np.asarray(u)
+    return np.ascontiguousarray(u.real), np.ascontiguousarray(u.imag)
+
+
+# ------------------------------------------------------------------ helpers
+
+
+def unit_slices(u0: int, ulen: int, n_z: int):
+    """Slice range [lo, hi) covered by pair units [u0, u0+ulen)."""
+    return 2 * u0, min(2 * (u0 + ulen), n_z)
+
+
+def rank_ranges(n_units: int, world: int):
+    """Contiguous pair-unit range per rank: plan_chunks semantics in one pass
+    (equal lengths, trailing ranks one shorter)."""
+    per = max(1, math.ceil(n_units / world))
+    return list(plan_chunks(n_units, world, per).passes[0])
+
+
+def _failure(stat, n_units, n_z, workers, max_per_pass, causes):
+    """First failing unit -> WorkerFailureError over the task holding it
+    (pipeline.py:166-176, 215-217)."""
+    bad = [u for u in range(n_units) if stat[u] != 0]
+    if not bad:
+        return None
+    u = bad[0]
+    plan = plan_chunks(n_units, workers, max(1, max_per_pass // 2))
+    for start, ln in plan.nonempty_ranges():
+        if start <= u < start + ln:
+            return WorkerFailureError(unit_slices(start, ln, n_z), causes.get(u, "failed"))
+    return WorkerFailureError(unit_slices(u, 1, n_z), causes.get(u, "failed"))
+
+
+def _cause(code: int, algo: str) -> str:
+    from . import _lib
+    name = {_lib.ERR_DIVERGENCE: "DivergenceError", _lib.ERR_NONFINITE: "NonFiniteError"}.get(
+        code, "SptomoError")
+    return f"{name}('{algo} failed on the device (status {code})')"
+
+
+def _device_solver(ops, cfg):
+    """(slices tensor/array (k, T, P)) -> (rec, final residual, iters, conv, status) per unit."""
+    from .solvers import solve_batch
+
+    def run(data):
+        rec, reps, stat = solve_batch(data, ops, cfg, raise_on_failure=False)
+        final = [r.residual_history[-1] if r.residual_history else 0.0 for r in reps]
+        iters = [r.iterations_run for r in reps]
+        conv = [r.converged for r in reps]
+        return rec, final, iters, conv, stat
+    return run
+
+
+def run_pipeline(stack: SinogramStack, cfg, workers: int = 1, ops=None, max_per_pass: int = 8,
+                 *, group=None, solver=None):
+    """Reconstruct every slice (pipeline.py:179-235).
+
+    Single process: all pair units go through the device solver in batches
+    (``workers`` / ``max_per_pass`` only define the task ranges reported by
+    WorkerFailureError, exactly as in the reference).  Under an initialised
+    torch.distributed group of size G > 1, rank r solves its contiguous unit
+    range on its own GPU; rank 0 returns the assembled stack, other ranks
+    return ``(None, report)``.  ``solver`` overrides the per-rank solve
+    (used by the CPU multi-process tests).
+    """
+    t0 = time.perf_counter()
+    geom = stack.geometry
+    if ops is None and solver is None:
+        from .operators import build_operators
+        ops = build_operators(geom, filter_kind=cfg.filter_kind())
+    solve_fn = solver or _device_solver(ops, cfg)
+    n_z = stack.n_z
+    n_units = (n_z + 1) // 2
+
+    dist = _dist_group(group)
+    if dist is None:
+        rec, final, iters, conv, stat = solve_fn(stack.data)
+        err = _failure(stat, n_units, n_z, workers, max_per_pass,
+                       {u: _cause(stat[u], cfg.algorithm) for u in range(n_units)})
+        if err is not None:
+            raise err
+        out = np.asarray(rec, dtype=np.float64)
+        from .solvers import SolverReport
+        rep = SolverReport(residual_history=[float(f) for f in final],
+                           iterations_run=int(max(iters)) if iters else 0,
+                           converged=all(conv), wall_time=time.perf_counter() - t0)
+        return TomogramStack(data=out), rep
+    return _run_distributed(stack, cfg, solve_fn, dist, t0, workers, max_per_pass)
+
+
+def _dist_group(group):
+    try:
+        import torch.distributed as tdist
+    except Exception:
+        return None
+    if not (tdist.is_available() and tdist.is_initialized()):
+        return None
+    if tdist.get_world_size(group) <= 1:
+        return None
+    return group if group is not None else tdist.group.WORLD
+
+
+def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass):
+    import torch
+    import torch.distributed as tdist
+
+    from .solvers import SolverReport
+
+    rank, world = tdist.get_rank(group), tdist.get_world_size(group)
+    backend = tdist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    geom = stack.geometry
+    n_z = stack.n_z
+    n_units = (n_z + 1) // 2
+    T, P = geom.sino_shape
+    Y, X = geom.grid_shape
+    ranges = rank_ranges(n_units, world)
+    spans = [unit_slices(u0, ul, n_z) if ul > 0 else (0, 0) for u0, ul in ranges]
+
+    # ---- scatter: rank 0 -> ranks (NCCL P2P over NVLink; no native scatter)
+    lo, hi = spans[rank]
+    mine = torch.empty((hi - lo, T, P), dtype=torch.float32, device=dev)
+    ops_ = []
+    if rank == 0:
+        full = torch.from_numpy(np.ascontiguousarray(stack.data, dtype=np.float32)).to(dev)
+        for r in range(1, world):
+            a, b = spans[r]
+            if b > a:
+                ops_.append(tdist.P2POp(tdist.isend, full[a:b].contiguous(), r, group))
+        mine.copy_(full[lo:hi])
+    elif hi > lo:
+        ops_.append(tdist.P2POp(tdist.irecv, mine, 0, group))
+    if ops_:
+        for w in tdist.batch_isend_irecv(ops_):
+            w.wait()
+
+    # ---- solve (no collective inside)
+    ul = ranges[rank][1]
+    if ul > 0:
+        rec, final, iters, conv, stat = solve_fn(mine)
+        rec = torch.as_tensor(rec, device=dev).to(torch.float32)
+    else:
+        rec = torch.empty((0, Y, X), dtype=torch.float32, device=dev)
+        final, iters, conv, stat = [], [], [], []
+    meta = torch.tensor([[f, i, float(c), float(s)] for f, i, c, s in zip(final, iters, conv, stat)],
+                        dtype=torch.float64, device=dev).reshape(-1, 4)
+
+    # ---- gather: ranks -> rank 0
+    ops_ = []
+    if rank == 0:
+        vol = torch.empty((n_z, Y, X), dtype=torch.float32, device=dev)
+        metas = [None] * world
+        vol[lo:hi].copy_(rec)
+        metas[0] = meta
+        for r in range(1, world):
+            a, b = spans[r]
+            if b > a:
+                buf = vol[a:b]
+                ops_.append(tdist.P2POp(tdist.irecv, buf, r, group))
+                metas[r] = torch.empty((ranges[r][1], 4), dtype=torch.float64, device=dev)
+                ops_.append(tdist.P2POp(tdist.irecv, metas[r], r, group))
+    elif hi > lo:
+        ops_.append(tdist.P2POp(tdist.isend, rec.contiguous(), 0, group))
+        ops_.append(tdist.P2POp(tdist.isend, meta, 0, group))
+    if ops_:
+        for w in tdist.batch_isend_irecv(ops_):
+            w.wait()
+
+    # ---- failure decision is shared so every rank raises the same error
+    flag = torch.zeros(3, dtype=torch.float64, device=dev)
+    if rank == 0:
+        allm = torch.cat([m for m in metas if m is not None]).cpu().numpy()
+        stat_all = allm[:, 3].astype(int)
+        bad = np.flatnonzero(stat_all)
+        if bad.size:
+            u = int(bad[0])
+            r = next(i for i, (u0, ln) in enumerate(ranges) if u0 <= u < u0 + ln)
+            flag[0], flag[1], flag[2] = 1.0, float(r), float(stat_all[u])
+    tdist.broadcast(flag, 0, group)
+    if flag[0].item() > 0:
+        r = int(flag[1].item())
+        raise WorkerFailureError(spans[r], _cause(int(flag[2].item()), cfg.algorithm))
+    if rank != 0:
+        return None, SolverReport(wall_time=time.perf_counter() - t0)
+    rep = SolverReport(residual_history=[float(v) for v in allm[:, 0]],
+                       iterations_run=int(allm[:, 1].max()) if len(allm) else 0,
+                       converged=bool(np.all(allm[:, 2] > 0)),
+                       wall_time=time.perf_counter() - t0)
+    return TomogramStack(data=vol.cpu().numpy().astype(np.float64)), rep

@@ -1,0 +1,169 @@
+"""Generate golden fixtures from the UNMODIFIED reference package.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``sptomo`` read-only from /root/reference/pkg/src and writes
+``tests/golden/*.npz``.  The fixtures travel with the repo; the reference does
+not (it is absent on the GPU box).  Nothing here is imported by the product.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import zlib
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+# (name, ScanGeometry kwargs, KernelSpec kwargs)
+GEOMS = [
+    ("g32", dict(n_p=32, n_theta=20), {}),
+    ("godd", dict(n_p=33, n_theta=17, center=15.7), {}),
+    ("grect", dict(n_p=24, n_theta=11, n_x=28, n_y=20), {}),
+    ("gw5", dict(n_p=32, n_theta=16), dict(width=5)),
+    ("ggauss", dict(n_p=32, n_theta=16), dict(family="gauss")),
+    ("gangles", dict(n_p=16, n_theta=5,
+                     angles=np.array([0.3, 1.1, 2.0, 3.7, 5.9])), {}),
+    ("c1", dict(n_p=256, n_theta=180), {}),
+]
+
+FILTERS = ("ramlak", "hamming", "shepplogan")
+
+
+def _phantom_like(sp, geom):
+    n = min(geom.n_x, geom.n_y)
+    img = np.zeros(geom.grid_shape)
+    ph = sp.phantom_shepp_logan(n)[0]
+    img[:n, :n] = ph
+    return img
+
+
+def operators_case(sp, name, gkw, kkw):
+    geom = sp.ScanGeometry(**gkw)
+    kern = sp.KernelSpec(**kkw)
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    ops = sp.build_operators(geom, kernel=kern, filter_kind="none")
+    u = _phantom_like(sp, geom)
+    lite = geom.n_grid > 20000  # config-1 size: phantom-derived inputs only
+    if lite:
+        # complex pair = (phantom, 0.5 * transposed phantom); sino = radon(u)
+        uc = u + 0.5j * u.T
+        s = ops.radon(u)
+        sc = ops.radon(uc)
+    else:
+        uc = rng.standard_normal(geom.grid_shape) + 1j * rng.standard_normal(geom.grid_shape)
+        s = rng.standard_normal(geom.sino_shape)
+        sc = rng.standard_normal(geom.sino_shape) + 1j * rng.standard_normal(geom.sino_shape)
+    out = dict(
+        n_p=geom.n_p, n_theta=geom.n_theta, n_x=geom.n_x, n_y=geom.n_y,
+        center=geom.center, angles=geom.angles,
+        k_family=kern.family, k_width=kern.width, k_beta=kern.beta, k_sigma=kern.sigma,
+        nnz=ops.csr.nnz, deapo=ops.deapo.values,
+        u=u, uc=uc, s=s, sc=sc,
+        radon_u=ops.radon(u), radon_uc=ops.radon(uc),
+        adj_s=ops.radon_adjoint(s), adj_sc=ops.radon_adjoint(sc),
+        S_row_ptr=ops.csr.row_ptr.astype(np.int64),
+        SH_row_ptr=ops.csr.adj_row_ptr.astype(np.int64),
+        S_abs_sum=float(np.abs(ops.csr.vals).sum()),
+        S_val_sum=complex(ops.csr.vals.sum()),
+    )
+    small = geom.n_samples * 9 < 20000
+    if small:
+        out.update(S_col_idx=ops.csr.col_idx, S_vals=ops.csr.vals,
+                   SH_col_idx=ops.csr.adj_col_idx, SH_vals=ops.csr.adj_vals)
+    if lite:
+        # drop fields the consumer can recompute bit-exactly
+        for key in ("s", "sc", "uc"):
+            out.pop(key)
+        out["S_row_ptr"] = out["S_row_ptr"].astype(np.int32)
+        out["SH_row_ptr"] = out["SH_row_ptr"].astype(np.int32)
+    for kind in (FILTERS[:1] if lite else FILTERS):
+        fops = sp.build_operators(geom, kernel=kern, filter_kind=kind)
+        out[f"calib_{kind}"] = fops.calib_scale
+        out[f"iradon_{kind}_radon_u"] = fops.iradon(out["radon_u"])
+        if not lite:
+            out[f"iradon_{kind}_s"] = fops.iradon(s)
+            out[f"apply_{kind}_s"] = fops.apply_weights(s)
+            out[f"apply_{kind}_sc"] = fops.apply_weights(sc)
+    return out
+
+
+def solvers_case(sp):
+    """Paired / separate solver runs on the test_solvers.py:354-368 setup."""
+    geom = sp.ScanGeometry(n_p=32, n_theta=20)
+    yy, xx = np.mgrid[0:32, 0:32]
+    a = np.clip(14 - np.hypot(xx - 16, yy - 16), 0, 1) * 0.8
+    b = (np.hypot(xx - 12, yy - 18) < 6).astype(float)
+    out = dict(slice_a=a, slice_b=b)
+    rng = np.random.default_rng(5)
+    for algo, iters in (("fbp", 1), ("sirt", 8), ("cgls", 8), ("tv", 5)):
+        cfg = sp.SolverConfig(algorithm=algo, max_iter=iters)
+        ops = sp.build_operators(geom, filter_kind=cfg.filter_kind())
+        sa = ops.radon(a)
+        sb = ops.radon(b) + 0.01 * rng.standard_normal(geom.sino_shape)
+        out[f"{algo}_sino_a"] = sa
+        out[f"{algo}_sino_b"] = sb
+        rp, rep_p = sp.solve(sp.pair_complex(sa, sb), ops, cfg)
+        ra, rep_a = sp.solve(sa, ops, cfg)
+        out[f"{algo}_rec_pair"] = rp
+        out[f"{algo}_rec_a"] = ra
+        out[f"{algo}_hist_pair"] = np.asarray(rep_p.residual_history)
+        out[f"{algo}_hist_a"] = np.asarray(rep_a.residual_history)
+        out[f"{algo}_iters_pair"] = rep_p.iterations_run
+        out[f"{algo}_conv_pair"] = rep_p.converged
+    # nonneg / no-BB / tol variants
+    ops_h = sp.build_operators(geom, filter_kind="hamming")
+    sa = out["sirt_sino_a"]
+    for tag, cfg in (("sirt_nobb", sp.SolverConfig(algorithm="sirt", max_iter=6, bb_enabled=False)),
+                     ("sirt_nonneg", sp.SolverConfig(algorithm="sirt", max_iter=6, nonneg=True)),
+                     ("sirt_tol", sp.SolverConfig(algorithm="sirt", max_iter=50, tol=0.05))):
+        r, rep = sp.solve(sa, ops_h, cfg)
+        out[f"{tag}_rec"] = r
+        out[f"{tag}_hist"] = np.asarray(rep.residual_history)
+        out[f"{tag}_iters"] = rep.iterations_run
+    ops_n = sp.build_operators(geom, filter_kind="none")
+    cfg = sp.SolverConfig(algorithm="tv", max_iter=3, mu=0.5, filter="none")
+    r, rep = sp.solve(out["tv_sino_a"], ops_n, cfg)
+    out["tv_mu_rec"] = r
+    out["tv_mu_hist"] = np.asarray(rep.residual_history)
+    return out
+
+
+def pipeline_case(sp):
+    """run_pipeline on an odd 5-slice stack (test_pipeline.py:131-136)."""
+    geom = sp.ScanGeometry(n_p=32, n_theta=12, n_z=5)
+    ops = sp.build_operators(geom, filter_kind="ramlak")
+    yy, xx = np.mgrid[0:32, 0:32]
+    data = np.stack([ops.radon(np.clip(12 - np.hypot(xx - 16, yy - 16), 0, 1) * (1.0 - 0.05 * k))
+                     for k in range(5)])
+    stack = sp.SinogramStack(data=data, geometry=geom)
+    out = {"stack": data}
+    for algo, iters in (("fbp", 1), ("sirt", 4)):
+        cfg = sp.SolverConfig(algorithm=algo, max_iter=iters)
+        o = sp.build_operators(geom, filter_kind=cfg.filter_kind())
+        vol, rep = sp.run_pipeline(stack, cfg, ops=o)
+        out[f"{algo}_vol"] = vol.data
+        out[f"{algo}_res"] = np.asarray(rep.residual_history)
+        out[f"{algo}_iters"] = rep.iterations_run
+    return out
+
+
+def main():
+    sys.path.insert(0, REF)
+    import sptomo as sp  # noqa: E402  (the unmodified reference)
+    for name, gkw, kkw in GEOMS:
+        d = operators_case(sp, name, gkw, kkw)
+        np.savez_compressed(os.path.join(OUT, f"ops_{name}.npz"), **d)
+        print("wrote", name, "nnz", d["nnz"])
+    np.savez_compressed(os.path.join(OUT, "solvers_g32.npz"), **solvers_case(sp))
+    np.savez_compressed(os.path.join(OUT, "pipeline_g32.npz"), **pipeline_case(sp))
+    print("done")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,106 @@
+"""Pin the CPU oracle against golden vectors from the unmodified reference."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_geom, load_golden, rel
+from oracle import (build_gridding, build_oracle_ops, deapodization, o_solve,
+                    op_apply_weights, filter_weights, OGeom, OracleOps)
+
+OPS_FILES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "ops_*.npz")))
+
+
+@pytest.fixture(scope="module", params=OPS_FILES)
+def case(request):
+    d = load_golden(request.param)
+    g, k = golden_geom(d)
+    return d, g, k, build_oracle_ops(g, k, "none")
+
+
+def test_matrix_structure(case):
+    d, g, k, ops = case
+    assert ops.grid.nnz == int(d["nnz"])
+    np.testing.assert_array_equal(ops.grid.S.indptr, d["S_row_ptr"])
+    np.testing.assert_array_equal(ops.grid.SH.indptr, d["SH_row_ptr"])
+    if "S_col_idx" in d:
+        np.testing.assert_array_equal(ops.grid.S.indices, d["S_col_idx"])
+        np.testing.assert_array_equal(ops.grid.SH.indices, d["SH_col_idx"])
+        np.testing.assert_allclose(ops.grid.S.data, d["S_vals"], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(ops.grid.SH.data, d["SH_vals"], rtol=0, atol=1e-15)
+    assert abs(np.abs(ops.grid.S.data).sum() - float(d["S_abs_sum"])) <= 1e-9 * float(d["S_abs_sum"])
+
+
+def test_deapodization(case):
+    d, g, k, ops = case
+    np.testing.assert_allclose(ops.deapo, d["deapo"], rtol=1e-13, atol=0)
+
+
+def test_radon_and_adjoint(case):
+    d, g, k, ops = case
+    assert rel(ops.radon(d["u"]), d["radon_u"]) <= 1e-12
+    assert rel(ops.radon(_uc(d)), d["radon_uc"]) <= 1e-12
+    assert rel(ops.radon_adjoint(_s(d, ops)), d["adj_s"]) <= 1e-12
+    assert rel(ops.radon_adjoint(_sc(d, ops)), d["adj_sc"]) <= 1e-12
+
+
+def _uc(d):
+    return d["uc"] if "uc" in d else d["u"] + 0.5j * d["u"].T
+
+
+def _s(d, ops):
+    return d["s"] if "s" in d else ops.radon(d["u"])
+
+
+def _sc(d, ops):
+    return d["sc"] if "sc" in d else ops.radon(_uc(d))
+
+
+@pytest.mark.parametrize("kind", ["ramlak", "hamming", "shepplogan"])
+def test_filtered_iradon_and_calibration(case, kind):
+    d, g, k, _ = case
+    if f"calib_{kind}" not in d:
+        pytest.skip("fixture carries ramlak only at this size")
+    fops = build_oracle_ops(g, k, kind)
+    assert abs(fops.calib - float(d[f"calib_{kind}"])) <= 1e-12 * abs(fops.calib)
+    assert rel(fops.iradon(d["radon_u"]), d[f"iradon_{kind}_radon_u"]) <= 1e-11
+    if f"iradon_{kind}_s" in d:
+        assert rel(fops.iradon(d["s"]), d[f"iradon_{kind}_s"]) <= 1e-11
+        assert rel(fops.apply_weights(d["s"]), d[f"apply_{kind}_s"]) <= 1e-13
+        assert rel(fops.apply_weights(d["sc"]), d[f"apply_{kind}_sc"]) <= 1e-13
+
+
+@pytest.fixture(scope="module")
+def sol():
+    return load_golden("solvers_g32.npz")
+
+
+@pytest.mark.parametrize("algo,iters", [("fbp", 1), ("sirt", 8), ("cgls", 8), ("tv", 5)])
+def test_solvers_match_reference(sol, algo, iters):
+    kind = {"fbp": "ramlak", "sirt": "hamming", "cgls": "none", "tv": "none"}[algo]
+    ops = build_oracle_ops(OGeom(n_p=32, n_theta=20), kind=kind)
+    sa, sb = sol[f"{algo}_sino_a"], sol[f"{algo}_sino_b"]
+    rp, rep_p = o_solve(sa + 1j * sb, ops, algo, max_iter=iters)
+    ra, rep_a = o_solve(sa, ops, algo, max_iter=iters)
+    assert rel(rp, sol[f"{algo}_rec_pair"]) <= 1e-10
+    assert rel(ra, sol[f"{algo}_rec_a"]) <= 1e-10
+    np.testing.assert_allclose(rep_p.history, sol[f"{algo}_hist_pair"], rtol=1e-10)
+    np.testing.assert_allclose(rep_a.history, sol[f"{algo}_hist_a"], rtol=1e-10)
+    assert rep_p.iterations == int(sol[f"{algo}_iters_pair"])
+
+
+def test_solver_variants(sol):
+    ops = build_oracle_ops(OGeom(n_p=32, n_theta=20), kind="hamming")
+    sa = sol["sirt_sino_a"]
+    for tag, kw in (("sirt_nobb", dict(max_iter=6, bb=False)),
+                    ("sirt_nonneg", dict(max_iter=6, nonneg=True)),
+                    ("sirt_tol", dict(max_iter=50, tol=0.05))):
+        r, rep = o_solve(sa, ops, "sirt", **kw)
+        assert rel(r, sol[f"{tag}_rec"]) <= 1e-10, tag
+        assert rep.iterations == int(sol[f"{tag}_iters"]), tag
+        np.testing.assert_allclose(rep.history, sol[f"{tag}_hist"], rtol=1e-10)
+    opn = build_oracle_ops(OGeom(n_p=32, n_theta=20), kind="none")
+    r, rep = o_solve(sol["tv_sino_a"], opn, "tv", max_iter=3, mu=0.5)
+    assert rel(r, sol["tv_mu_rec"]) <= 1e-10
