@@ -1,12 +1,1274 @@
-// Device-resident solvers (placeholder until the fused solver kernels land).
+// Device-resident batched solvers: FBP, SIRT (BB steps), CGLS, split-Bregman TV.
+//
+// Restates solvers.py:122-460 for a batch of B complex units (each = two real
+// slices = two channels, solvers.py:1-10).  Formulation choices:
+//  * Sinogram-space vectors live in the detector-frequency domain in the
+//    batch-innermost layout [s][b]:  Rhat = FFT1(r).  Because
+//    FFT1(radon(v)) = S^H FFT2(deapo v) exactly (unnormalised FFTs, the
+//    reference's gamma collapses to 1/n_p -- SURVEY Appendix A.2), the 1D FFT
+//    pair of every "r = b - A u" / "A^H W r" step cancels: an iteration costs
+//    one FFT2 + one IFFT2 + two SpMMs.
+//  * Per-channel weighted norms come from one complex spectrum by the
+//    Hermitian split |F(re)|^2, |F(im)|^2 = (A +- C)/(2 n_p), with
+//    A = sum w|R_k|^2, C = sum w Re(R_k R_-k)  (needs symmetric w, which
+//    every radial filter is).  Per-channel scaling of a spectral vector mixes
+//    bins k and -k (mirror kernel below).
+//  * Every scalar of the reference (alpha, beta, gamma, delta, mu, tol,
+//    divergence, activity) is computed on the device per unit and channel;
+//    reductions are fixed-shape two-stage trees (deterministic, independent
+//    of a unit's position in the batch).  The host only polls a lagged
+//    "units still active" counter to stop early.
+//  * Precision: the operators (SpMM, cuFFT, their fused epilogues) run in the
+//    plan precision R.  SIRT recomputes r = b - A u every iteration, so its
+//    iterates stay in R.  The Krylov recurrences of CGLS and TV (u, p, r,
+//    and TV's d / b / grad residuals) are carried in float64 -- exactly the
+//    "fp32 operator outputs, fp64 vectors" regime the survey measured
+//    against the 1e-3 solver bar (hard part 6).
 #include "sptb_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace sptb {
+
+template <typename R> struct CT;
+template <> struct CT<float> { using T = float2; };
+template <> struct CT<double> { using T = double2; };
+using D2 = double2;
+
+enum UnitStatus { RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_NONFINITE = 3,
+                  ST_ZERO = 4, ST_STOPPED = 5, ST_PAD = 6 };
+
+struct Unit {
+    double alpha[2], alpha0[2], beta[2], gamma[2], gamma0[2], bnorm[2];
+    double mu[2], lam[2];
+    double min_res;
+    int act[2];      // per-channel activity of the current CG step
+    int status;      // UnitStatus
+    int active;      // still iterating (outer loop)
+    int stepped;     // took a step this iteration
+    int iters;
+    int single;      // real input: channel 1 absent
+    int converged;
+    int inner_stop;  // TV inner CGLS: break flag
+    int pad_;
+};
+
+struct Global {
+    int n_active;
+};
+
+// ------------------------------------------------------------------ reductions
+
+constexpr int RT = 256;
+
+template <int K, bool MAX>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[K], double* out) {
+    __shared__ double sh[K > 0 ? K : 1][RT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double v = acc[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double t = __shfl_down_sync(0xffffffffu, v, o);
+            v = MAX ? fmax(v, t) : v + t;
+        }
+        if (lane == 0) sh[k][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double s = MAX ? 0.0 : 0.0;
+        for (int w = 0; w < RT / 32; ++w) s = MAX ? fmax(s, sh[threadIdx.x][w]) : s + sh[threadIdx.x][w];
+        out[threadIdx.x] = s;
+    }
+}
+
+// partial[(blk*B + b)*K + k] -> sums[b*K + k], fixed order over blk
+__global__ void k_finish(const double* __restrict__ part, int nblk, int B, int K, int is_max,
+                         double* __restrict__ sums) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * K) return;
+    const int b = i / K, k = i % K;
+    double s = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+        const double v = part[((size_t)blk * B + b) * K + k];
+        s = is_max ? fmax(s, v) : s + v;
+    }
+    sums[i] = s;
+}
+
+// grid kernels: gridDim = (nblk, B); block-uniform unit b; element (b, m)
+struct GridIdx {
+    int X, Y;
+};
+
+template <int K, bool MAX, class Op>
+__global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
+    const int b = blockIdx.y;
+    double acc[K > 0 ? K : 1];
+#pragma unroll
+    for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0;
+    if (op.enabled(b)) {
+        const long long stride = (long long)gridDim.x * RT;
+        for (long long m = blockIdx.x * (long long)RT + threadIdx.x; m < M; m += stride)
+            op(b, (size_t)b * M + m, m, acc);
+    }
+    if constexpr (K > 0) block_reduce_store<K, MAX>(acc, part + ((size_t)blockIdx.x * gridDim.y + b) * K);
+}
+
+// ------------------------------------------------------------------ helpers
+
+template <typename T>
+__device__ __forceinline__ T pos_(T v) { return v > (T)0 ? v : (T)0; }
+
+__device__ __forceinline__ bool finite2(double x, double y) { return isfinite(x) && isfinite(y); }
+
+__device__ __forceinline__ double safe_div(double num, double den, double fb) {
+    return den > 0 ? num / den : fb;
+}
+
+template <typename C>
+__device__ __forceinline__ D2 d2(const C& c) { return make_double2((double)c.x, (double)c.y); }
+
+template <typename R>
+__device__ __forceinline__ typename CT<R>::T rc(double x, double y) {
+    typename CT<R>::T c;
+    c.x = (R)x;
+    c.y = (R)y;
+    return c;
+}
+
+// forward differences (solvers.py:308-314): last column / row zero
+__device__ __forceinline__ D2 grad_x(const D2* v, size_t i, long long m, int X) {
+    if ((int)(m % X) == X - 1) return make_double2(0, 0);
+    const D2 a = v[i], b = v[i + 1];
+    return make_double2(b.x - a.x, b.y - a.y);
+}
+__device__ __forceinline__ D2 grad_y(const D2* v, size_t i, long long m, int X, int Y) {
+    if ((int)(m / X) == Y - 1) return make_double2(0, 0);
+    const D2 a = v[i], b = v[i + X];
+    return make_double2(b.x - a.x, b.y - a.y);
+}
+// -div2d(vx, vy) (solvers.py:317-327), i.e. grad^T
+__device__ __forceinline__ D2 grad_t(const D2* vx, const D2* vy, size_t i, long long m, int X,
+                                     int Y) {
+    // div2d(vx,vy)[y][x] = vx[x] (x<X-1) - vx[x-1] (x>0) + same along y; return its negative
+    const int x = (int)(m % X), y = (int)(m / X);
+    double re = 0, im = 0;
+    if (x < X - 1) { re += vx[i].x; im += vx[i].y; }
+    if (x > 0) { re -= vx[i - 1].x; im -= vx[i - 1].y; }
+    if (y < Y - 1) { re += vy[i].x; im += vy[i].y; }
+    if (y > 0) { re -= vy[i - X].x; im -= vy[i - X].y; }
+    return make_double2(-re, -im);
+}
+
+// ------------------------------------------------------------------ grid ops (SIRT / FBP)
+
+template <typename R>
+struct OpSirtUpdate {  // u += alpha g; [nonneg]; W = deapo u; count non-finite u
+    using C = typename CT<R>::T;
+    C* u;
+    const C* g;
+    C* w;
+    const R* deapo;
+    const Unit* us;
+    int nonneg;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
+        C x = u[i];
+        const Unit& un = us[b];
+        if (un.active) {
+            const C gg = g[i];
+            x.x = (R)((double)x.x + un.alpha[0] * (double)gg.x);
+            x.y = (R)((double)x.y + un.alpha[1] * (double)gg.y);
+            if (nonneg) {
+                x.x = pos_(x.x);
+                x.y = pos_(x.y);
+            }
+            u[i] = x;
+        }
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+        const R d = deapo[m];
+        w[i] = rc<R>(x.x * d, x.y * d);
+    }
+};
+
+template <typename R, typename V>
+struct OpDeapo {  // w = deapo * v * scale  (v of any precision, w of plan precision)
+    using C = typename CT<R>::T;
+    const V* v;
+    C* w;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
+        const D2 x = d2(v[i]);
+        const double d = (double)deapo[m] * scale;
+        w[i] = rc<R>(x.x * d, x.y * d);
+    }
+};
+
+template <typename R, typename V>
+struct OpStore {  // out = deapo * y * scale  (V precision)
+    using C = typename CT<R>::T;
+    const C* y;
+    V* out;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
+        const C yy = y[i];
+        const double d = (double)deapo[m] * scale;
+        V o;
+        o.x = yy.x * d;
+        o.y = yy.y * d;
+        out[i] = o;
+    }
+};
+
+// g = deapo*y*scale (adjoint post-IFFT2); acc <g,g> per channel; with BB the
+// dots vs the previous g: <du,du> = a^2 <g,g>, <du, g - g_new> = a <g, g - g_new>
+template <typename R, bool BB>
+struct OpAdjPost {
+    using C = typename CT<R>::T;
+    const C* y;
+    C* g;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&acc)[BB ? 4 : 2]) const {
+        const C yy = y[i];
+        const double d = (double)deapo[m] * scale;
+        const C gn = rc<R>(yy.x * d, yy.y * d);
+        if (BB) {
+            const C go = g[i];
+            acc[0] += (double)go.x * go.x;
+            acc[1] += (double)go.y * go.y;
+            acc[2] += (double)go.x * ((double)go.x - (double)gn.x);
+            acc[3] += (double)go.y * ((double)go.y - (double)gn.y);
+        } else {
+            acc[0] += (double)gn.x * gn.x;
+            acc[1] += (double)gn.y * gn.y;
+        }
+        g[i] = gn;
+    }
+};
+
+template <typename V>
+struct OpNonfinite {
+    const V* u;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long, double (&acc)[1]) const {
+        const D2 x = d2(u[i]);
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+    }
+};
+
+template <typename V>
+struct OpNonneg {
+    V* u;
+    const Unit* us;
+    __device__ bool enabled(int b) const { return us[b].status != ST_PAD; }
+    __device__ void operator()(int, size_t i, long long, double (&)[1]) const {
+        V x = u[i];
+        x.x = pos_(x.x);
+        x.y = pos_(x.y);
+        u[i] = x;
+    }
+};
+
+template <typename R>
+struct OpAbsMax {  // per-channel max |deapo*y*scale| (TV default mu, solvers.py:364-372)
+    using C = typename CT<R>::T;
+    const C* y;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
+        const C yy = y[i];
+        const double d = (double)deapo[m] * scale;
+        acc[0] = fmax(acc[0], fabs((double)(R)(yy.x * d)));
+        acc[1] = fmax(acc[1], fabs((double)(R)(yy.y * d)));
+    }
+};
+
+// ------------------------------------------------------------------ grid ops (CGLS, fp64 vectors)
+
+template <typename R>
+struct OpCglsInit {  // p = s = deapo*y*scale ; <s,s> ; W = deapo p
+    using C = typename CT<R>::T;
+    C* w;
+    D2* p;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
+        const C yy = w[i];
+        const double d = (double)deapo[m];
+        const D2 s = make_double2(yy.x * d * scale, yy.y * d * scale);
+        acc[0] += s.x * s.x;
+        acc[1] += s.y * s.y;
+        p[i] = s;
+        w[i] = rc<R>(s.x * d, s.y * d);
+    }
+};
+
+template <typename R>
+struct OpDotS {  // <s,s>, s = deapo*y*scale
+    using C = typename CT<R>::T;
+    const C* y;
+    const R* deapo;
+    double scale;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
+        const C yy = y[i];
+        const double d = (double)deapo[m] * scale;
+        const double sx = yy.x * d, sy = yy.y * d;
+        acc[0] += sx * sx;
+        acc[1] += sy * sy;
+    }
+};
+
+template <typename R>
+struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-finite u
+    using C = typename CT<R>::T;
+    D2* u;
+    D2* p;
+    C* w;  // in: y (IFFT2 output), out: deapo * p
+    const R* deapo;
+    double scale;
+    const Unit* us;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
+        const Unit& un = us[b];
+        D2 x = u[i];
+        D2 pp = p[i];
+        const double d = (double)deapo[m];
+        if (un.stepped) {
+            x.x += un.alpha[0] * pp.x;
+            x.y += un.alpha[1] * pp.y;
+            u[i] = x;
+            if (un.active) {
+                const C yy = w[i];
+                pp.x = yy.x * d * scale + un.beta[0] * pp.x;
+                pp.y = yy.y * d * scale + un.beta[1] * pp.y;
+                p[i] = pp;
+            }
+        }
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+        w[i] = rc<R>(pp.x * d, pp.y * d);
+    }
+};
+
+// ------------------------------------------------------------------ grid ops (TV)
+
+// rho = (d - b) - grad u  (the stacked target minus fwd(u), unscaled; solvers.py:410-411,438)
+struct OpTvRho {
+    const D2 *u, *dx, *dy, *bx, *by;
+    D2 *rx, *ry;
+    int X, Y;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
+        const D2 gx = grad_x(u, i, m, X), gy = grad_y(u, i, m, X, Y);
+        rx[i] = make_double2(dx[i].x - bx[i].x - gx.x, dx[i].y - bx[i].y - gx.y);
+        ry[i] = make_double2(dy[i].x - by[i].x - gy.x, dy[i].y - by[i].y - gy.y);
+    }
+};
+
+// s = mu (deapo y scale) + lam grad^T(rho)   (adj(), solvers.py:397-399)
+// MODE 0: p = s, W = deapo p, acc <s,s>;  1: acc <s,s>;  2: p = s + beta p, W = deapo p
+template <typename R, int MODE>
+struct OpTvS {
+    using C = typename CT<R>::T;
+    C* w;
+    D2* p;
+    const D2 *rx, *ry;
+    const R* deapo;
+    double scale;
+    const Unit* us;
+    int X, Y;
+    __device__ bool enabled(int b) const { return MODE == 1 || us[b].active; }
+    __device__ void operator()(int b, size_t i, long long m, double (&acc)[2]) const {
+        const Unit& un = us[b];
+        const C yy = w[i];
+        const double d = (double)deapo[m];
+        const D2 gt = grad_t(rx, ry, i, m, X, Y);
+        const D2 s = make_double2(un.mu[0] * (yy.x * d * scale) + un.lam[0] * gt.x,
+                                  un.mu[1] * (yy.y * d * scale) + un.lam[1] * gt.y);
+        if (MODE <= 1) {
+            acc[0] += s.x * s.x;
+            acc[1] += s.y * s.y;
+        }
+        if (MODE == 0) {
+            p[i] = s;
+            w[i] = rc<R>(s.x * d, s.y * d);
+        }
+        if (MODE == 2) {
+            D2 pp = p[i];
+            if (!un.inner_stop) {
+                pp.x = s.x + un.beta[0] * pp.x;
+                pp.y = s.y + un.beta[1] * pp.y;
+                p[i] = pp;
+            }
+            w[i] = rc<R>(pp.x * d, pp.y * d);
+        }
+    }
+};
+
+struct OpTvGradNorm {  // ||grad p||^2 per channel
+    const D2* p;
+    const Unit* us;
+    int X, Y;
+    __device__ bool enabled(int b) const { return us[b].active; }
+    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
+        const D2 gx = grad_x(p, i, m, X), gy = grad_y(p, i, m, X, Y);
+        acc[0] += gx.x * gx.x + gy.x * gy.x;
+        acc[1] += gx.y * gx.y + gy.y * gy.y;
+    }
+};
+
+struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
+    D2 *u, *rx, *ry;
+    const D2* p;
+    const Unit* us;
+    int X, Y;
+    __device__ bool enabled(int b) const { return us[b].stepped; }
+    __device__ void operator()(int b, size_t i, long long m, double (&)[1]) const {
+        const Unit& un = us[b];
+        const D2 pp = p[i];
+        const D2 gx = grad_x(p, i, m, X), gy = grad_y(p, i, m, X, Y);
+        D2 x = u[i];
+        x.x += un.alpha[0] * pp.x;
+        x.y += un.alpha[1] * pp.y;
+        u[i] = x;
+        D2 a = rx[i], c = ry[i];
+        a.x -= un.alpha[0] * gx.x;
+        a.y -= un.alpha[1] * gx.y;
+        c.x -= un.alpha[0] * gy.x;
+        c.y -= un.alpha[1] * gy.y;
+        rx[i] = a;
+        ry[i] = c;
+    }
+};
+
+// isotropic shrink + Bregman update (solvers.py:418-421, 330-341); W = deapo u
+template <typename R>
+struct OpTvShrink {
+    using C = typename CT<R>::T;
+    const D2* u;
+    D2 *dx, *dy, *bx, *by;
+    C* w;
+    const R* deapo;
+    const Unit* us;
+    int X, Y;
+    __device__ bool enabled(int) const { return true; }
+    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
+        const Unit& un = us[b];
+        const D2 x = u[i];
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+        const double d = (double)deapo[m];
+        w[i] = rc<R>(x.x * d, x.y * d);
+        if (!un.active) return;
+        const D2 gx = grad_x(u, i, m, X), gy = grad_y(u, i, m, X, Y);
+        const D2 vbx = bx[i], vby = by[i];
+        const double vx[2] = {gx.x + vbx.x, gx.y + vbx.y};
+        const double vy[2] = {gy.x + vby.x, gy.y + vby.y};
+        double ox[2], oy[2];
+        for (int c = 0; c < 2; ++c) {
+            const double kap = 1.0 / un.lam[c];
+            const double mag = sqrt(vx[c] * vx[c] + vy[c] * vy[c]);
+            const double f = fmax(mag - kap, 0.0) / (mag > 0 ? mag : 1.0);
+            ox[c] = vx[c] * f;
+            oy[c] = vy[c] * f;
+        }
+        dx[i] = make_double2(ox[0], ox[1]);
+        dy[i] = make_double2(oy[0], oy[1]);
+        bx[i] = make_double2(vbx.x + gx.x - ox[0], vbx.y + gx.y - ox[1]);
+        by[i] = make_double2(vby.x + gy.x - oy[0], vby.y + gy.y - oy[1]);
+    }
+};
+
+// ------------------------------------------------------------------ spectral kernels
+// Pairs (t, jh) with its mirror (t, (P-jh) mod P), all b.  UPDATE: Rhat -=
+// chan_scale(alpha, Qhat) through the mirror mix (stepped units only); then the
+// A, C partial sums of the (updated) Rhat.  RV = storage of Rhat; rf = optional
+// plan-precision copy of Rhat for the next SpMM.
+template <typename R, typename RV, bool UPDATE>
+__global__ void __launch_bounds__(RT)
+k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
+       typename CT<R>::T* __restrict__ rf, const R* __restrict__ w, long long wlen, int T, int P,
+       int B, const Unit* __restrict__ us, double* __restrict__ part) {
+    const int H = P / 2 + 1;
+    const long long total = (long long)T * H * B;
+    const long long stride = (long long)gridDim.x * RT;
+    double a = 0, c = 0;
+    const int b = threadIdx.x % B;  // RT and stride are multiples of B
+    const bool step = UPDATE ? (us[b].stepped != 0) : false;
+    double ap = 0, am = 0;
+    if (UPDATE) {
+        ap = 0.5 * (us[b].alpha[0] + us[b].alpha[1]);
+        am = 0.5 * (us[b].alpha[0] - us[b].alpha[1]);
+    }
+    for (long long idx = blockIdx.x * (long long)RT + threadIdx.x; idx < total; idx += stride) {
+        const long long q = idx / B;
+        const int t = (int)(q / H), jh = (int)(q % H);
+        const int j1 = jh, j2 = (P - jh) % P;
+        if (j1 > j2 && j2 != 0) continue;  // odd P: each pair once
+        const size_t s1 = (size_t)t * P + j1, s2 = (size_t)t * P + j2;
+        const double wt = w ? (double)(wlen == P ? w[j1] : w[s1]) : 1.0;
+        D2 r1 = d2(rh[s1 * B + b]);
+        D2 r2 = d2(rh[s2 * B + b]);
+        if (UPDATE && step) {
+            const D2 q1 = d2(qh[s1 * B + b]), q2 = d2(qh[s2 * B + b]);
+            const D2 n1 = make_double2(r1.x - (ap * q1.x + am * q2.x), r1.y - (ap * q1.y - am * q2.y));
+            const D2 n2 = make_double2(r2.x - (ap * q2.x + am * q1.x), r2.y - (ap * q2.y - am * q1.y));
+            r1 = n1;
+            r2 = n2;
+            RV o1, o2;
+            o1.x = r1.x; o1.y = r1.y;
+            o2.x = r2.x; o2.y = r2.y;
+            rh[s1 * B + b] = o1;
+            if (j2 != j1) rh[s2 * B + b] = o2;
+        }
+        if (rf) {
+            rf[s1 * B + b] = rc<R>(r1.x, r1.y);
+            if (j2 != j1) rf[s2 * B + b] = rc<R>(r2.x, r2.y);
+        }
+        if (j1 == j2) {
+            a += wt * (r1.x * r1.x + r1.y * r1.y);
+            c += wt * (r1.x * r1.x - r1.y * r1.y);
+        } else {
+            a += wt * (r1.x * r1.x + r1.y * r1.y + r2.x * r2.x + r2.y * r2.y);
+            c += 2.0 * wt * (r1.x * r2.x - r1.y * r2.y);
+        }
+    }
+    // reduce threads sharing b (tid = b + B*k), fixed order
+    __shared__ double sa[RT], sc[RT];
+    sa[threadIdx.x] = a;
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x < B) {
+        double ta = 0, tc = 0;
+        for (int k = threadIdx.x; k < RT; k += B) {
+            ta += sa[k];
+            tc += sc[k];
+        }
+        double* o = part + ((size_t)blockIdx.x * B + threadIdx.x) * 2;
+        o[0] = ta;
+        o[1] = tc;
+    }
+}
+
+template <typename A, typename Bt>
+__global__ void k_convert(const A* __restrict__ src, Bt* __restrict__ dst, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Bt o;
+        o.x = src[i].x;
+        o.y = src[i].y;
+        dst[i] = o;
+    }
+}
+
+// ------------------------------------------------------------------ scalar kernels
+// A, C -> per-channel squared weighted norms
+__device__ __forceinline__ void chan_norm2(const double* ac, int P, const Unit& un, double* n2) {
+    n2[0] = fmax((ac[0] + ac[1]) / (2.0 * P), 0.0);
+    n2[1] = un.single ? 0.0 : fmax((ac[0] - ac[1]) / (2.0 * P), 0.0);
+}
+
+__global__ void k_init_units(Unit* us, int nb, int B, int single_last, Global* gl) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit u;
+    memset(&u, 0, sizeof(Unit));
+    u.min_res = INFINITY;
+    u.status = b < nb ? RUNNING : ST_PAD;
+    u.active = b < nb;
+    u.single = (single_last && b == nb - 1) ? 1 : 0;
+    us[b] = u;
+    if (b == 0) gl->n_active = 0;
+}
+
+// b_norm per channel; zero right-hand side -> converged, 0 iterations
+__global__ void k_bnorm(Unit* us, const double* ac, int P, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (un.status == ST_PAD) return;
+    double n2[2];
+    chan_norm2(ac + 2 * b, P, un, n2);
+    un.bnorm[0] = sqrt(n2[0]);
+    un.bnorm[1] = sqrt(n2[1]);
+    if (sqrt(n2[0] + n2[1]) == 0.0) {
+        un.status = ST_ZERO;
+        un.active = 0;
+        un.converged = 1;
+    }
+}
+
+// residual bookkeeping shared by FBP / SIRT / CGLS / TV
+// (solvers.py:127-129, 164-176, 214-221, 422-428)
+__device__ void record_residual(Unit& un, const double* ac, int P, int it, int B, int b,
+                                double* hist, bool nonfinite, bool divergence, double tol,
+                                bool tol_only_positive) {
+    double n2[2];
+    chan_norm2(ac, P, un, n2);
+    const double r0 = sqrt(n2[0]), r1 = sqrt(n2[1]);
+    const double res = sqrt(n2[0] + n2[1]);
+    hist[(size_t)it * B + b] = res;
+    un.iters += 1;
+    if (nonfinite) {
+        un.status = ST_NONFINITE;
+        un.active = 0;
+        un.converged = 0;
+        return;
+    }
+    if (divergence) {
+        if (res < un.min_res) un.min_res = res;  // python min(): NaN never wins
+        if (res > 10.0 * un.min_res) {
+            un.status = ST_DIVERGED;
+            un.active = 0;
+            return;
+        }
+    }
+    const double rel = fmax(safe_div(r0, un.bnorm[0], 0.0), safe_div(r1, un.bnorm[1], 0.0));
+    if ((!tol_only_positive || tol > 0) && rel <= tol) {
+        un.status = ST_CONVERGED;
+        un.converged = 1;
+        un.active = 0;
+    }
+}
+
+__global__ void k_count_active(const Unit* us, int B, Global* gl) {
+    __shared__ int n;
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+    if (threadIdx.x < B && us[threadIdx.x].active) atomicAdd(&n, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) gl->n_active = n;
+}
+
+__global__ void k_fbp_check(Unit* us, const double* ac, const double* nf, int P, int B,
+                            double* hist) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (un.status == ST_PAD) return;
+    record_residual(un, ac + 2 * b, P, 0, B, b, hist, nf[b] > 0, false, -1.0, false);
+    if (un.status != ST_NONFINITE) {
+        un.status = ST_CONVERGED;
+        un.converged = 1;
+    }
+}
+
+// SIRT: alpha0 = <g,g> / ||A g||_w^2  (solvers.py:152-156)
+__global__ void k_sirt_alpha0(Unit* us, const double* gg, const double* ac, int P, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    double n2[2];
+    chan_norm2(ac + 2 * b, P, un, n2);
+    for (int c = 0; c < 2; ++c) {
+        const double a0 = (un.single && c == 1) ? 0.0 : safe_div(gg[2 * b + c], n2[c], 0.0);
+        un.alpha0[c] = a0;
+        un.alpha[c] = un.active ? a0 : 0.0;
+    }
+}
+
+__global__ void k_sirt_check(Unit* us, const double* ac, const double* nf, int P, int it, int B,
+                             double* hist, double tol) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (!un.active) return;
+    record_residual(un, ac + 2 * b, P, it, B, b, hist, nf[b] > 0, true, tol, false);
+}
+
+// BB1 step with safeguarded fallback (solvers.py:177-184)
+__global__ void k_sirt_alpha(Unit* us, const double* dots, int B, int bb) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    for (int c = 0; c < 2; ++c) {
+        double a = un.alpha0[c];
+        if (bb && !(un.single && c == 1)) {
+            const double al = un.alpha[c];
+            const double dd = al * al * dots[4 * b + c];
+            const double ddg = al * dots[4 * b + 2 + c];
+            a = safe_div(dd, ddg, un.alpha0[c]);
+            if (!(a > 0)) a = un.alpha0[c];
+        }
+        if (un.single && c == 1) a = 0.0;
+        un.alpha[c] = un.active ? a : 0.0;
+    }
+}
+
+// CGLS (solvers.py:197-226)
+__global__ void k_cgls_init(Unit* us, const double* ss, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    for (int c = 0; c < 2; ++c) {
+        un.gamma[c] = ss[2 * b + c];
+        un.gamma0[c] = un.gamma[c];
+    }
+}
+
+// delta = ||q||^2 per channel.  tv != 0: stacked TV delta = mu ||A p||_w^2 +
+// lam ||grad p||^2 (solvers.py:401-403,444-451), non-finite guard, no gamma floor.
+__global__ void k_cgls_alpha(Unit* us, const double* ac, const double* gnorm, int P, int B, int tv) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    un.stepped = 0;
+    const bool live = tv ? (un.active && !un.inner_stop) : un.active;
+    un.alpha[0] = un.alpha[1] = 0.0;
+    if (!live) return;
+    double dl[2];
+    chan_norm2(ac + 2 * b, P, un, dl);
+    if (tv)
+        for (int c = 0; c < 2; ++c)
+            dl[c] = (un.single && c == 1) ? 0.0 : un.mu[c] * dl[c] + un.lam[c] * gnorm[2 * b + c];
+    if (tv && !(isfinite(dl[0]) && isfinite(dl[1]) && isfinite(un.gamma[0]) &&
+                isfinite(un.gamma[1]))) {
+        un.status = ST_NONFINITE;
+        un.active = 0;
+        return;
+    }
+    const double eps2 = 2.220446049250313e-16 * 2.220446049250313e-16;
+    bool any = false;
+    for (int c = 0; c < 2; ++c) {
+        bool a = dl[c] > 0;
+        if (!tv) a = a && (un.gamma[c] > eps2 * un.gamma0[c]);
+        if (un.single && c == 1) a = false;
+        un.act[c] = a;
+        any = any || a;
+    }
+    if (!any) {
+        if (tv) {
+            un.inner_stop = 1;
+        } else {
+            un.status = ST_STOPPED;  // breakdown / stagnation: flagged, not thrown
+            un.active = 0;
+        }
+        return;
+    }
+    for (int c = 0; c < 2; ++c) un.alpha[c] = un.act[c] ? safe_div(un.gamma[c], dl[c], 0.0) : 0.0;
+    un.stepped = 1;
+}
+
+__global__ void k_cgls_check(Unit* us, const double* ac, int P, int it, int B, double* hist,
+                             double tol) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (!un.stepped) return;
+    record_residual(un, ac + 2 * b, P, it, B, b, hist, false, false, tol, false);
+}
+
+__global__ void k_cgls_beta(Unit* us, const double* ss, int B, int tv) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (!un.stepped) {
+        un.beta[0] = un.beta[1] = 0.0;
+        return;
+    }
+    for (int c = 0; c < 2; ++c) {
+        un.beta[c] = un.act[c] ? safe_div(ss[2 * b + c], un.gamma[c], 0.0) : 0.0;
+        un.gamma[c] = ss[2 * b + c];
+    }
+    (void)tv;
+}
+
+// non-finite u after a step overrides the tol decision (solvers.py:217 precedes :219)
+__global__ void k_flag_nonfinite(Unit* us, const double* nf, int B, int only_stepped) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (un.status == ST_PAD) return;
+    if (only_stepped && !un.stepped) return;
+    if (nf[b] > 0 && un.status != ST_NONFINITE) {
+        un.status = ST_NONFINITE;
+        un.active = 0;
+        un.converged = 0;
+    }
+}
+
+// TV: mu per channel (cfg or 0.1 max|A^H b|), lam = 2 mu  (solvers.py:364-375)
+__global__ void k_tv_mu(Unit* us, const double* mx, double cfg_mu, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    for (int c = 0; c < 2; ++c) {
+        double mu = cfg_mu > 0 ? cfg_mu : 0.1 * mx[2 * b + c];
+        if (!(mu > 0)) mu = 1.0;
+        if (un.single && c == 1) mu = cfg_mu > 0 ? cfg_mu : un.mu[0];
+        un.mu[c] = mu;
+        un.lam[c] = 2.0 * mu;
+    }
+    if (un.single && cfg_mu <= 0) {  // channel 1 copies channel 0 (kappa[-1], solvers.py:338)
+        un.mu[1] = un.mu[0];
+        un.lam[1] = un.lam[0];
+    }
+}
+
+__global__ void k_tv_inner_begin(Unit* us, const double* ss, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    un.inner_stop = 0;
+    un.gamma[0] = ss[2 * b];
+    un.gamma[1] = ss[2 * b + 1];
+}
+
+__global__ void k_tv_check(Unit* us, const double* ac, const double* nf, int P, int it, int B,
+                           double* hist, double tol) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (!un.active) return;
+    if (nf[b] > 0) {  // _check_finite(u, "tv") precedes the residual (solvers.py:417)
+        un.status = ST_NONFINITE;
+        un.active = 0;
+        return;
+    }
+    record_residual(un, ac + 2 * b, P, it, B, b, hist, false, false, tol, true);
+}
+
+__global__ void k_tv_finish(Unit* us, int B) {  // for/else: full run counts as converged
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    if (un.status == RUNNING) {
+        un.status = ST_CONVERGED;
+        un.converged = 1;
+        un.active = 0;
+    }
+}
+
+// ------------------------------------------------------------------ host driver
+
+template <typename R>
+struct Solver {
+    using C = typename CT<R>::T;
+    sptb_plan* p;
+    int B;
+    cudaStream_t st;
+    int nblk_grid = 0, nblk_spec = 0;
+    // plan precision
+    C *U = nullptr, *G = nullptr, *W = nullptr, *BH = nullptr, *RH = nullptr, *QH = nullptr;
+    // float64 Krylov state (CGLS / TV)
+    D2 *Ud = nullptr, *Pd = nullptr, *RHd = nullptr;
+    D2 *dx = nullptr, *dy = nullptr, *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;
+    double *part = nullptr, *sums = nullptr, *sums2 = nullptr, *sums3 = nullptr, *hist = nullptr;
+    Unit* us = nullptr;
+    Global* gl = nullptr;
+    int* pinned = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    std::vector<void*> owned;
+
+    int alloc(void** ptr, size_t bytes) {
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SPTB_ERR_OOM, "solver buffers: out of device memory");
+        }
+        owned.push_back(*ptr);
+        return SPTB_OK;
+    }
+    ~Solver() {
+        for (void* q : owned) cudaFree(q);
+        if (pinned) cudaFreeHost(pinned);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+
+    int init(int algo, int max_iter) {
+        st = p->stream;
+        SPTB_TRY(ensure_work(p, B));
+        const size_t gb = sizeof(C) * (size_t)B * p->M, sb = sizeof(C) * (size_t)B * p->N;
+        const size_t gd = sizeof(D2) * (size_t)B * p->M, sd = sizeof(D2) * (size_t)B * p->N;
+        W = (C*)p->G0;
+        SPTB_TRY(alloc((void**)&BH, sb));
+        SPTB_TRY(alloc((void**)&RH, sb));
+        SPTB_TRY(alloc((void**)&QH, sb));
+        if (algo == SPTB_ALGO_FBP || algo == SPTB_ALGO_SIRT) {
+            SPTB_TRY(alloc((void**)&U, gb));
+            SPTB_TRY(alloc((void**)&G, gb));
+        } else {
+            SPTB_TRY(alloc((void**)&Ud, gd));
+            SPTB_TRY(alloc((void**)&Pd, gd));
+            SPTB_TRY(alloc((void**)&RHd, sd));
+        }
+        if (algo == SPTB_ALGO_TV) {
+            for (D2** q : {&dx, &dy, &bx, &by, &rx, &ry}) SPTB_TRY(alloc((void**)q, gd));
+        }
+        nblk_grid = std::max(1, 1184 / B);
+        nblk_spec = 1184;
+        const size_t np = (size_t)std::max(nblk_grid, nblk_spec) * B * 4;
+        SPTB_TRY(alloc((void**)&part, sizeof(double) * np));
+        SPTB_TRY(alloc((void**)&sums, sizeof(double) * B * 4));
+        SPTB_TRY(alloc((void**)&sums2, sizeof(double) * B * 4));
+        SPTB_TRY(alloc((void**)&sums3, sizeof(double) * B * 4));
+        SPTB_TRY(alloc((void**)&hist, sizeof(double) * (size_t)std::max(max_iter, 1) * B));
+        SPTB_TRY(alloc((void**)&us, sizeof(Unit) * B));
+        SPTB_TRY(alloc((void**)&gl, sizeof(Global)));
+        SPTB_CUDA(cudaHostAlloc((void**)&pinned, sizeof(int) * 2, cudaHostAllocDefault));
+        for (auto& e : ev) SPTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return SPTB_OK;
+    }
+
+    int zero_state(int algo) {
+        const size_t gb = sizeof(C) * (size_t)B * p->M, gd = sizeof(D2) * (size_t)B * p->M;
+        if (U) SPTB_CUDA(cudaMemsetAsync(U, 0, gb, st));
+        if (Ud) SPTB_CUDA(cudaMemsetAsync(Ud, 0, gd, st));
+        if (algo == SPTB_ALGO_TV)
+            for (D2* q : {dx, dy, bx, by}) SPTB_CUDA(cudaMemsetAsync(q, 0, gd, st));
+        return SPTB_OK;
+    }
+
+    template <int K, bool MAX = false, class Op>
+    int grid(const Op& op, double* out_sums) {
+        dim3 g(nblk_grid, B);
+        k_grid<K, MAX, Op><<<g, RT, 0, st>>>(op, p->M, part);
+        SPTB_LAUNCHED();
+        if (K > 0 && out_sums) {
+            k_finish<<<(B * K + 127) / 128, 128, 0, st>>>(part, nblk_grid, B, K, MAX ? 1 : 0,
+                                                          out_sums);
+            SPTB_LAUNCHED();
+        }
+        return SPTB_OK;
+    }
+
+    template <bool UPDATE, typename RV>
+    int spec(RV* rh, const C* qh, C* rf, double* out_sums) {
+        k_spec<R, RV, UPDATE><<<nblk_spec, RT, 0, st>>>(rh, qh, rf, (const R*)p->w_dev, p->w_len,
+                                                        p->T, p->P, B, us, part);
+        SPTB_LAUNCHED();
+        k_finish<<<(B * 2 + 127) / 128, 128, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
+
+    int fft(cufftHandle h, void* z, int dir) {
+        count_launch();
+        if (sizeof(R) == 8)
+            SPTB_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)z, (cufftDoubleComplex*)z, dir));
+        else
+            SPTB_CUFFT(cufftExecC2C(h, (cufftComplex*)z, (cufftComplex*)z, dir));
+        return SPTB_OK;
+    }
+
+    // out[s][b] = (sub ? sub - : ) S^H FFT2(W)    (W holds deapo*v, [b][m]; clobbered)
+    int forward_spec(C* out, const C* sub) {
+        FFTPlans* f;
+        SPTB_TRY(get_fft(p, B, &f));
+        SPTB_TRY(fft(f->fft2, W, CUFFT_FORWARD));
+        const void* x = W;
+        if (B > 1) {
+            SPTB_TRY(launch_transpose_bm_to_mb<R>(W, p->G1, B, p->M, st));
+            x = p->G1;
+        }
+        return launch_spmm<R>(p->SH, p->SH.val, x, out, B, false, sub, st);
+    }
+
+    // W[b][m] = IFFT2(S_(w) rh)   (caller applies deapo/P)
+    int adjoint_grid(const C* rh, bool filtered) {
+        FFTPlans* f;
+        SPTB_TRY(get_fft(p, B, &f));
+        const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
+        SPTB_TRY(launch_spmm<R>(p->S, vals, rh, W, B, true, nullptr, st));
+        return fft(f->fft2, W, CUFFT_INVERSE);
+    }
+
+    // BH = FFT1(sino) in [s][b]; units from caller slices
+    int load_sino(const void* in, int fmt, int64_t n, int64_t u0, int nb) {
+        FFTPlans* f;
+        SPTB_TRY(get_fft(p, B, &f));
+        SPTB_TRY(launch_pack<R>(in, fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
+        SPTB_TRY(fft(f->fft1, p->S0, CUFFT_FORWARD));
+        if (B > 1) return launch_transpose_bm_to_mb<R>(p->S0, BH, B, p->N, st);
+        SPTB_CUDA(cudaMemcpyAsync(BH, p->S0, sizeof(C) * p->N, cudaMemcpyDeviceToDevice, st));
+        return SPTB_OK;
+    }
+
+    int unit_kernel_done() {
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
+
+    // lagged early exit: true when every unit had stopped one iteration ago
+    int poll(int it, bool* stop) {
+        *stop = false;
+        k_count_active<<<1, 64, 0, st>>>(us, B, gl);
+        SPTB_LAUNCHED();
+        SPTB_CUDA(cudaMemcpyAsync(pinned + (it & 1), &gl->n_active, sizeof(int),
+                                  cudaMemcpyDeviceToHost, st));
+        SPTB_CUDA(cudaEventRecord(ev[it & 1], st));
+        if (it >= 1) {
+            SPTB_CUDA(cudaEventSynchronize(ev[(it - 1) & 1]));
+            if (pinned[(it - 1) & 1] == 0) *stop = true;
+        }
+        return SPTB_OK;
+    }
+
+    const R* deapo() const { return (const R*)p->deapo; }
+
+    // ---------------------------------------------------------------- FBP
+    int run_fbp() {
+        const bool filt = p->SW_val != nullptr;
+        const double scale = (filt ? p->calib : 1.0) / p->P;
+        SPTB_TRY(adjoint_grid(BH, filt));
+        SPTB_TRY(grid<0>(OpStore<R, C>{W, U, deapo(), scale}, nullptr));
+        // weighted residual of the reprojection (solvers.py:125-128)
+        SPTB_TRY(grid<0>(OpDeapo<R, C>{U, W, deapo(), 1.0}, nullptr));
+        SPTB_TRY(forward_spec(RH, BH));
+        SPTB_TRY(grid<1>(OpNonfinite<C>{U}, sums2));
+        SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
+        k_fbp_check<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, hist);
+        return unit_kernel_done();
+    }
+
+    // ---------------------------------------------------------------- SIRT
+    int run_sirt(const sptb_solver_config& cfg) {
+        const double invP = 1.0 / p->P;
+        // g = A^H W b ; alpha0 from ||A g||_w  (solvers.py:151-156)
+        SPTB_TRY(adjoint_grid(BH, true));
+        SPTB_TRY(grid<2>(OpAdjPost<R, false>{W, G, deapo(), invP}, sums2));
+        SPTB_TRY(grid<0>(OpDeapo<R, C>{G, W, deapo(), 1.0}, nullptr));
+        SPTB_TRY(forward_spec(QH, nullptr));
+        SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
+        k_sirt_alpha0<<<1, 64, 0, st>>>(us, sums2, sums, p->P, B);
+        SPTB_TRY(unit_kernel_done());
+        for (int it = 0; it < cfg.max_iter; ++it) {
+            bool stop;
+            SPTB_TRY(poll(it, &stop));
+            if (stop) break;
+            // u += alpha g ; W = deapo u ; non-finite count
+            SPTB_TRY(grid<1>(OpSirtUpdate<R>{U, G, W, deapo(), us, cfg.nonneg}, sums2));
+            SPTB_TRY(forward_spec(RH, BH));  // Rhat = Bhat - F(u)
+            SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
+            k_sirt_check<<<1, 64, 0, st>>>(us, sums, sums2, p->P, it, B, hist, cfg.tol);
+            SPTB_TRY(unit_kernel_done());
+            // g_new = A^H W r ; BB dots against the previous g
+            SPTB_TRY(adjoint_grid(RH, true));
+            SPTB_TRY(grid<4>(OpAdjPost<R, true>{W, G, deapo(), invP}, sums3));
+            k_sirt_alpha<<<1, 64, 0, st>>>(us, sums3, B, cfg.bb_enabled);
+            SPTB_TRY(unit_kernel_done());
+        }
+        return SPTB_OK;
+    }
+
+    int copy_bh_to_rhd() {
+        const long long n = (long long)B * p->N;
+        k_convert<C, D2><<<(int)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, st>>>(BH, RHd, n);
+        return unit_kernel_done();
+    }
+
+    // ---------------------------------------------------------------- CGLS
+    int run_cgls(const sptb_solver_config& cfg) {
+        const double invP = 1.0 / p->P;
+        // r = b (u0 = 0); s = A^H W r; p = s; gamma = <s,s>  (solvers.py:197-203)
+        SPTB_TRY(copy_bh_to_rhd());
+        SPTB_TRY(adjoint_grid(BH, true));
+        SPTB_TRY(grid<2>(OpCglsInit<R>{W, Pd, deapo(), invP}, sums2));
+        k_cgls_init<<<1, 64, 0, st>>>(us, sums2, B);
+        SPTB_TRY(unit_kernel_done());
+        for (int it = 0; it < cfg.max_iter; ++it) {
+            bool stop;
+            SPTB_TRY(poll(it, &stop));
+            if (stop) break;
+            // q = A p  -> delta, alpha, activity
+            SPTB_TRY(forward_spec(QH, nullptr));
+            SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
+            k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, nullptr, p->P, B, 0);
+            SPTB_TRY(unit_kernel_done());
+            // r -= alpha q (mirror mix, fp64) and ||r||_w ; RH = plan-precision copy
+            SPTB_TRY(spec<true>(RHd, QH, RH, sums));
+            k_cgls_check<<<1, 64, 0, st>>>(us, sums, p->P, it, B, hist, cfg.tol);
+            SPTB_TRY(unit_kernel_done());
+            // s = A^H W r ; gamma_new ; beta
+            SPTB_TRY(adjoint_grid(RH, true));
+            SPTB_TRY(grid<2>(OpDotS<R>{W, deapo(), invP}, sums2));
+            k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 0);
+            SPTB_TRY(unit_kernel_done());
+            // u += alpha p ; p = s + beta p ; W = deapo p_new
+            SPTB_TRY(grid<1>(OpCglsTail<R>{Ud, Pd, W, deapo(), invP, us}, sums3));
+            k_flag_nonfinite<<<1, 64, 0, st>>>(us, sums3, B, 1);
+            SPTB_TRY(unit_kernel_done());
+        }
+        if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
+        return SPTB_OK;
+    }
+
+    // ---------------------------------------------------------------- TV
+    int run_tv(const sptb_solver_config& cfg) {
+        const double invP = 1.0 / p->P;
+        const int X = p->X, Y = p->Y;
+        // mu: cfg or 0.1 max |A^H b| per channel (unfiltered adjoint)
+        if (cfg.mu > 0) {
+            k_tv_mu<<<1, 64, 0, st>>>(us, sums3, cfg.mu, B);
+        } else {
+            SPTB_TRY(adjoint_grid(BH, false));
+            SPTB_TRY((grid<2, true>(OpAbsMax<R>{W, deapo(), invP}, sums3)));
+            k_tv_mu<<<1, 64, 0, st>>>(us, sums3, 0.0, B);
+        }
+        SPTB_TRY(unit_kernel_done());
+        // u0 = 0 -> rho_a = b
+        SPTB_TRY(copy_bh_to_rhd());
+        SPTB_CUDA(cudaMemcpyAsync(RH, BH, sizeof(C) * (size_t)B * p->N, cudaMemcpyDeviceToDevice, st));
+        const int inner = std::max(1, cfg.tv_inner_iter);
+        for (int it = 0; it < cfg.max_iter; ++it) {
+            bool stop;
+            SPTB_TRY(poll(it, &stop));
+            if (stop) break;
+            // stacked CGLS on (sqrt(mu) A; sqrt(lam) grad) u = (sqrt(mu) b; sqrt(lam)(d - b))
+            SPTB_TRY(grid<0>(OpTvRho{Ud, dx, dy, bx, by, rx, ry, X, Y}, nullptr));
+            SPTB_TRY(adjoint_grid(RH, true));
+            SPTB_TRY(grid<2>(OpTvS<R, 0>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, sums2));
+            k_tv_inner_begin<<<1, 64, 0, st>>>(us, sums2, B);
+            SPTB_TRY(unit_kernel_done());
+            for (int j = 0; j < inner; ++j) {
+                SPTB_TRY(forward_spec(QH, nullptr));                // Qhat = F(p)
+                SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
+                SPTB_TRY(grid<2>(OpTvGradNorm{Pd, us, X, Y}, sums2));
+                k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
+                SPTB_TRY(unit_kernel_done());
+                SPTB_TRY(spec<true>(RHd, QH, RH, sums));             // rho_a -= alpha A p
+                SPTB_TRY(grid<0>(OpTvStep{Ud, rx, ry, Pd, us, X, Y}, nullptr));
+                SPTB_TRY(adjoint_grid(RH, true));
+                SPTB_TRY(grid<2>(OpTvS<R, 1>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, sums2));
+                k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 1);
+                SPTB_TRY(unit_kernel_done());
+                SPTB_TRY(grid<2>(OpTvS<R, 2>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, nullptr));
+            }
+            if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
+            // shrink + Bregman; W = deapo u; non-finite u
+            SPTB_TRY(grid<1>(OpTvShrink<R>{Ud, dx, dy, bx, by, W, deapo(), us, X, Y}, sums3));
+            // residual b - A u (reused as the next outer rho_a: same u)
+            SPTB_TRY(forward_spec(RH, BH));
+            SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
+            k_tv_check<<<1, 64, 0, st>>>(us, sums, sums3, p->P, it, B, hist, cfg.tol);
+            SPTB_TRY(unit_kernel_done());
+            const long long n = (long long)B * p->N;
+            k_convert<C, D2><<<(int)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, st>>>(RH, RHd, n);
+            SPTB_TRY(unit_kernel_done());
+        }
+        k_tv_finish<<<1, 64, 0, st>>>(us, B);
+        return unit_kernel_done();
+    }
+};
+
+template <typename R>
+int solve_typed(sptb_plan* p, const sptb_solver_config& cfg, const void* sino, int in_fmt,
+                void* rec, int out_fmt, int64_t n, double* hist, int32_t* iters,
+                int32_t* converged, int32_t* status) {
+    using C = typename CT<R>::T;
+    const bool cplx = in_fmt & SPTB_FMT_COMPLEX;
+    const int64_t units = cplx ? n : (n + 1) / 2;
+    const int iters_cap = cfg.algorithm == SPTB_ALGO_FBP ? 1 : cfg.max_iter;
+    int first_fail = SPTB_OK;
+    bool din = true, dout = true;
+    is_device_ptr(sino, &din);
+    is_device_ptr(rec, &dout);
+    const size_t eb = (in_fmt & SPTB_FMT_F64) ? 8 : 4, ebo = (out_fmt & SPTB_FMT_F64) ? 8 : 4;
+    const size_t per_in = eb * p->N * (cplx ? 2 : 1), per_out = ebo * p->M * (cplx ? 2 : 1);
+    const void* src = sino;
+    void* dst = rec;
+    if (!din) {
+        SPTB_TRY(ensure_stage(&p->stage_in, &p->stage_in_bytes, per_in * n));
+        SPTB_CUDA(cudaMemcpyAsync(p->stage_in, sino, per_in * n, cudaMemcpyHostToDevice, p->stream));
+        src = p->stage_in;
+    }
+    if (!dout) {
+        SPTB_TRY(ensure_stage(&p->stage_out, &p->stage_out_bytes, per_out * n));
+        dst = p->stage_out;
+    }
+    int Bmax = 1;
+    while (Bmax < std::min<int64_t>(units, p->max_batch)) Bmax <<= 1;
+    Solver<R> sv;
+    sv.p = p;
+    sv.B = Bmax;
+    SPTB_TRY(sv.init(cfg.algorithm, iters_cap));
+    std::vector<double> hbuf((size_t)iters_cap * Bmax);
+    std::vector<Unit> ubuf(Bmax);
+    for (int64_t u0 = 0; u0 < units; u0 += Bmax) {
+        const int nb = (int)std::min<int64_t>(Bmax, units - u0);
+        const bool single_last = !cplx && (2 * (u0 + nb) > n);
+        cudaStream_t st = p->stream;
+        k_init_units<<<1, 64, 0, st>>>(sv.us, nb, Bmax, single_last ? 1 : 0, sv.gl);
+        SPTB_LAUNCHED();
+        SPTB_TRY(sv.zero_state(cfg.algorithm));
+        SPTB_CUDA(cudaMemsetAsync(sv.hist, 0, sizeof(double) * (size_t)iters_cap * Bmax, st));
+        SPTB_TRY(sv.load_sino(src, in_fmt, n, u0, nb));
+        if (cfg.algorithm != SPTB_ALGO_FBP) {  // solve_fbp has no zero-rhs shortcut
+            SPTB_TRY(sv.template spec<false>(sv.BH, (const C*)nullptr, (C*)nullptr, sv.sums));
+            k_bnorm<<<1, 64, 0, st>>>(sv.us, sv.sums, p->P, Bmax);
+            SPTB_LAUNCHED();
+        }
+        switch (cfg.algorithm) {
+            case SPTB_ALGO_FBP: SPTB_TRY(sv.run_fbp()); break;
+            case SPTB_ALGO_SIRT: SPTB_TRY(sv.run_sirt(cfg)); break;
+            case SPTB_ALGO_CGLS: SPTB_TRY(sv.run_cgls(cfg)); break;
+            case SPTB_ALGO_TV: SPTB_TRY(sv.run_tv(cfg)); break;
+            default: return fail(SPTB_ERR_ARG, "unknown algorithm");
+        }
+        if (sv.Ud)
+            SPTB_TRY(launch_unpack<double>(sv.Ud, p->M, nullptr, 1.0, dst, out_fmt, n, u0, nb, st));
+        else
+            SPTB_TRY(launch_unpack<R>(sv.U, p->M, nullptr, 1.0, dst, out_fmt, n, u0, nb, st));
+        SPTB_CUDA(cudaMemcpyAsync(hbuf.data(), sv.hist, sizeof(double) * hbuf.size(),
+                                  cudaMemcpyDeviceToHost, st));
+        SPTB_CUDA(cudaMemcpyAsync(ubuf.data(), sv.us, sizeof(Unit) * Bmax, cudaMemcpyDeviceToHost, st));
+        SPTB_CUDA(cudaStreamSynchronize(st));
+        for (int b = 0; b < nb; ++b) {
+            const int64_t u = u0 + b;
+            const Unit& un = ubuf[b];
+            if (iters) iters[u] = un.iters;
+            if (converged) converged[u] = un.converged;
+            int s = SPTB_OK;
+            if (un.status == ST_DIVERGED) s = SPTB_ERR_DIVERGENCE;
+            if (un.status == ST_NONFINITE) s = SPTB_ERR_NONFINITE;
+            if (status) status[u] = s;
+            if (s != SPTB_OK && first_fail == SPTB_OK) {
+                first_fail = s;
+                fail(s, std::string(s == SPTB_ERR_DIVERGENCE ? "residual exceeds 10x its minimum"
+                                                             : "produced non-finite values") +
+                            " (unit " + std::to_string(u) + ")");
+            }
+            if (hist)
+                for (int k = 0; k < iters_cap; ++k)
+                    hist[u * iters_cap + k] = k < un.iters ? hbuf[(size_t)k * Bmax + b] : 0.0;
+        }
+    }
+    if (!dout) {
+        SPTB_CUDA(cudaMemcpyAsync(rec, dst, per_out * n, cudaMemcpyDeviceToHost, p->stream));
+        SPTB_CUDA(cudaStreamSynchronize(p->stream));
+    }
+    return first_fail;
+}
+
+}  // namespace sptb
 
 using namespace sptb;
 
 extern "C" int sptb_solve(sptb_plan* p, const sptb_solver_config* cfg, const void* sino,
                           int32_t in_fmt, void* rec, int32_t out_fmt, int64_t n, double* hist,
                           int32_t* iters, int32_t* converged, int32_t* status) {
-    (void)p; (void)cfg; (void)sino; (void)in_fmt; (void)rec; (void)out_fmt; (void)n;
-    (void)hist; (void)iters; (void)converged; (void)status;
-    return fail(SPTB_ERR_STATE, "sptb_solve: not implemented yet");
+    if (!p || !cfg) return fail(SPTB_ERR_ARG, "null argument");
+    if ((in_fmt & SPTB_FMT_COMPLEX) != (out_fmt & SPTB_FMT_COMPLEX))
+        return fail(SPTB_ERR_ARG, "output kind (real/complex) must match the input's");
+    if (cfg->max_iter < 1) return fail(SPTB_ERR_ARG, "max_iter must be >= 1");
+    if (cfg->algorithm < SPTB_ALGO_FBP || cfg->algorithm > SPTB_ALGO_TV)
+        return fail(SPTB_ERR_ARG, "unknown algorithm");
+    if (n <= 0) return SPTB_OK;
+    cudaSetDevice(p->device);
+    return p->prec == SPTB_PREC_F64
+               ? solve_typed<double>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
+                                     status)
+               : solve_typed<float>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
+                                    status);
 }

@@ -179,6 +179,9 @@ def test_zero_inputs(sb):
 
 
 def test_near_zero_deapodization_raises(sb):
+    # KB width 5, beta = 3 pi / 4: FT(K) has its first zero exactly at nu = 1/4,
+    # i.e. on the grid column n_x/2 + n_x/4 inside the support disk
+    import math
     with pytest.raises(sb.NearZeroDenominatorError):
         sb.build_operators(sb.ScanGeometry(n_p=16, n_theta=4),
-                           kernel=sb.KernelSpec(family="gauss", width=15, sigma=9.0))
+                           kernel=sb.KernelSpec(width=5, beta=0.75 * math.pi))
