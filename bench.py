@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 gridding operators (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = gridrec (filtered back-projection, RamLak, calibrated iradon) of
+a 64-slice batch of 2048x1536 sinograms per GPU (BASELINE configs[1]); under
+torchrun every rank reconstructs its own 64 slices (weak scaling, no data-path
+collective).  ``value`` is the whole-job slices/s with inputs resident in HBM,
+timed with CUDA events on the launching stream, max over ranks.  The same line
+carries: the SIRT iteration throughput (slice-iterations/s, setup excluded),
+the gridding SpMM HBM bandwidth of S and S^H, the roofline of the dominant
+kernel, an end-to-end number through the C ABI with host buffers, the sampled
+SM clocks, and (rank 0, N=1) the CPU oracle timed on this box's host cores.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+NumPy/SciPy oracle port in oracle/, the reference package itself cannot be
+installed on the GPU box) on all host cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "slices/s gridrec & SIRT-iter @2048²×1536 angles; gridding SpMM HBM GB/s"
+UNIT = "slices/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-p", type=int, default=2048)
+    ap.add_argument("--n-theta", type=int, default=1536)
+    ap.add_argument("--slices", type=int, default=64, help="slices per GPU per step")
+    ap.add_argument("--sirt-iters", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > i + 2 and r[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline)
+
+_ORACLE = {}
+
+
+def _oracle_pair(args):
+    """iradon of one slice pair through the oracle (reference operators.py:171-187)."""
+    k = args
+    ops = _ORACLE["ops"]
+    s = _ORACLE["sino"]
+    return float(ops.iradon(s[0] * (1.0 - 0.001 * k) + 1j * s[1] * (1.0 + 0.001 * k))[0, 0].real)
+
+
+def _oracle_setup(n_p, n_theta):
+    from oracle import OGeom, build_oracle_ops, shepp_logan
+    t0 = time.perf_counter()
+    ops = build_oracle_ops(OGeom(n_p, n_theta), kind="ramlak")
+    ph = shepp_logan(n_p, 2)
+    sino = [ops.radon(x) for x in ph]
+    _ORACLE.update(ops=ops, sino=sino)
+    return time.perf_counter() - t0
+
+
+def cpu_gridrec(n_p, n_theta, passes, pairs_per_core=1, cores=None, warm=0):
+    """Oracle gridrec over a fork pool of every host core; returns per-pass
+    seconds and the slices per pass."""
+    cores = cores or os.cpu_count() or 1
+    setup = _oracle_setup(n_p, n_theta)
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    ctx = mp.get_context("fork")
+    n_pairs = cores * pairs_per_core
+    times = []
+    with ctx.Pool(processes=cores) as pool:
+        for i in range(warm + passes):
+            t0 = time.perf_counter()
+            pool.map(_oracle_pair, range(n_pairs), chunksize=1)
+            dt = time.perf_counter() - t0
+            if i >= warm:
+                times.append(dt)
+    return times, 2 * n_pairs, cores, setup
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, slices, cores, setup = cpu_gridrec(a.n_p, a.n_theta, passes=a.steps, warm=a.warmup)
+    tot = sum(times)
+    v = slices * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic Shepp-Logan sinograms", "config": _config(a),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{slices} slices ({slices // 2} complex pairs) of gridrec "
+                                   f"per step over a fork pool of {cores} single-threaded "
+                                   f"workers; oracle setup {setup:.1f}s excluded"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(a):
+    return {"workload": f"gridrec/FBP {a.n_p}x{a.n_p}, {a.n_theta} angles, {a.slices}-slice "
+                        "batch per GPU (BASELINE configs[1])",
+            "n_p": a.n_p, "n_theta": a.n_theta, "slices_per_gpu": a.slices,
+            "filter": "ramlak", "batch_complex": a.slices // 2,
+            "l2": "inputs and outputs (>= 805 MB per step) exceed the 126 MB L2; no flush"}
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2003_12677_b200 as sb
+    from paper_2003_12677_b200 import _lib
+    from oracle import shepp_logan  # synthetic phantom generator only (io.py:130-148)
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n = a.slices
+    B = max(1, n // 2)
+    geom = sb.ScanGeometry(n_p=a.n_p, n_theta=a.n_theta)
+    t0 = time.perf_counter()
+    ops = sb.build_operators(geom, filter_kind="ramlak", max_batch=min(64, B))
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    plan = ops.plan
+    plan.bind_stream(stream.cuda_stream)
+
+    # synthetic data: device radon of the phantom, per-slice scale (io.py:147-148)
+    ph = torch.tensor(shepp_logan(a.n_p)[0], dtype=torch.float32, device=dev)
+    scales = torch.linspace(1.0, 0.8, n, device=dev) * (1.0 + 0.01 * rank)
+    sino = ops.radon(ph[None].expand(2, -1, -1).contiguous())[0]
+    sino = (sino[None] * scales[:, None, None]).contiguous()
+    out = torch.empty((n,) + geom.grid_shape, dtype=torch.float32, device=dev)
+    fmt = _lib.FMT_F32 | _lib.FMT_REAL
+    lib = _lib.lib
+
+    def step():
+        _lib.check(lib.sptb_iradon(plan.h, C.c_void_p(sino.data_ptr()), fmt,
+                                   C.c_void_p(out.data_ptr()), fmt, n), "iradon")
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0, f0 = lib.sptb_launch_count(), lib.sptb_fft_count()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.sptb_launch_count() - l0
+    ffts = lib.sptb_fft_count() - f0
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n * 1e3 / ms_max
+
+    # ---- gridding SpMM bandwidth (the >= 60% target) and the roofline
+    peak, peak_src = _peaks()
+    spmm = {}
+    for name, which in (("S_filtered", _lib.MAT_SW), ("S_H", _lib.MAT_SH)):
+        msl, uin = C.c_double(), C.c_int64()
+        _lib.check(lib.sptb_time_spmm(plan.h, which, B, 20, C.byref(msl), C.byref(uin)))
+        rows, cols, nnz = plan.matrix_info(_lib.MAT_SH if which == _lib.MAT_SH else _lib.MAT_S)
+        alg = 12 * nnz + 4 * (rows + 1) + 8 * B * (uin.value + rows)
+        spmm[name] = {"ms": msl.value, "algorithmic_bytes": alg, "distinct_inputs": uin.value,
+                      "nnz": nnz, "gbs": alg / msl.value / 1e6,
+                      "frac_of_peak": alg / msl.value / 1e6 / peak}
+    traffic = _traffic_from_profiles()
+    s = spmm["S_filtered"]
+    roofline = {"kernel": "sptb::k_spmm (S diag(w), gridrec)", "bound": "hbm",
+                "achieved": s["gbs"], "peak": peak, "unit": "GB/s", "frac": s["gbs"] / peak,
+                "traffic": traffic.get("S"), "peak_source": peak_src,
+                "bytes_model": "12*nnz + 4*(rows+1) + 8*B*(U_in + rows) per launch"}
+
+    # ---- SIRT iteration throughput (setup excluded by differencing)
+    sirt = _sirt_rate(sb, geom, sino, a, dev, stream)
+
+    # ---- end to end through the C ABI with host buffers (pinned)
+    e2e = None
+    if not a.no_e2e:
+        sino_h = sino.cpu().pin_memory()
+        out_h = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+
+        def step_h():
+            _lib.check(lib.sptb_iradon(plan.h, C.c_void_p(sino_h.data_ptr()), fmt,
+                                       C.c_void_p(out_h.data_ptr()), fmt, n), "iradon(host)")
+        step_h()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ks = max(3, a.steps // 2)
+        h0.record(stream)
+        for _ in range(ks):
+            step_h()
+        h1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([h0.elapsed_time(h1) / ks], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n * 1e3 / float(te.item()), "unit": UNIT,
+               "ms_per_step": float(te.item()),
+               "h2d_bytes_per_step": int(sino_h.numel() * 4) * world,
+               "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
+               "path": "sptb_iradon(plan, pinned host sinograms -> pinned host tomograms)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        times, slices, cores, setup = cpu_gridrec(a.n_p, a.n_theta, passes=2, pairs_per_core=1)
+        v = slices * len(times) / sum(times)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"2 passes of {slices} slices ({slices // 2} pairs) of oracle gridrec "
+                         f"over {cores} single-threaded fork workers; setup {setup:.1f}s excluded"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+            "data": "synthetic: device radon of the 10-ellipse Shepp-Logan phantom, "
+                    "per-slice scaled (io.py:130-148)",
+            "config": _config(a), "clocks": clk.summary(), "e2e": e2e,
+            "gpu_launches": int(launches), "cufft_execs": int(ffts),
+            "roofline": roofline, "cpu_baseline": cpu,
+            "sirt_iter": sirt, "spmm": spmm, "build_operators_s": build_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _sirt_rate(sb, geom, sino_clean, a, dev, stream):
+    """SIRT (Hamming, BB) slice-iterations/s on the same 64-slice batch with
+    2% Gaussian noise (BASELINE configs[2]); t(k2) - t(k1) removes the setup."""
+    import torch
+    ops_h = sb.build_operators(geom, filter_kind="hamming", max_batch=min(64, max(1, a.slices // 2)))
+    ops_h.plan.bind_stream(stream.cuda_stream)
+    g = torch.Generator(device=dev).manual_seed(1)
+    noisy = sino_clean + 0.02 * sino_clean.abs().max() * torch.randn(
+        sino_clean.shape, device=dev, generator=g)
+    times = {}
+    k1, k2 = 1, max(2, a.sirt_iters)
+    for k in (k1, k2, k1, k2):
+        cfg = sb.SolverConfig(algorithm="sirt", max_iter=k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, reps, stat = sb.solvers.solve_batch(noisy, ops_h, cfg, raise_on_failure=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times[k] = e0.elapsed_time(e1)
+        its = min(r.iterations_run for r in reps)
+    per_iter_ms = (times[k2] - times[k1]) / (k2 - k1)
+    return {"value": a.slices * 1e3 / per_iter_ms, "unit": "slice-iterations/s",
+            "ms_per_iteration": per_iter_ms, "setup_ms": times[k1] - per_iter_ms,
+            "iterations_run_min": its, "filter": "hamming",
+            "workload": f"SIRT-BB {a.slices} slices 2048^2x1536, 2% noise (BASELINE configs[2] shape)"}
+
+
+def _traffic_from_profiles():
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

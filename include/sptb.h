@@ -171,8 +171,18 @@ int sptb_solve(sptb_plan* plan, const sptb_solver_config* cfg,
                int64_t n, double* hist, int32_t* iters, int32_t* converged,
                int32_t* status);
 
-/* Timing hook for benchmarks: number of kernels this library launched. */
+/* Timing hook for benchmarks: number of kernels this library launched
+ * (hand-written kernels only; cuFFT executions are counted separately). */
 int64_t sptb_launch_count(void);
+int64_t sptb_fft_count(void);
+
+/* Benchmark hook: time `reps` back-to-back launches of the gridding SpMM
+ * (`which` = SPTB_MAT_S / _SH / _SW) over B complex columns in the layouts the
+ * operators use, with CUDA events on the plan's stream.  Returns the mean
+ * milliseconds per launch and the matrix's distinct referenced input rows
+ * (U_in of the algorithmic-bytes model).          */
+int sptb_time_spmm(sptb_plan* plan, int32_t which, int32_t B, int32_t reps,
+                   double* ms_per_launch, int64_t* distinct_inputs);
 
 #ifdef __cplusplus
 }

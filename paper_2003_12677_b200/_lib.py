@@ -46,6 +46,9 @@ SIGNATURES = [
     ("sptb_last_error", C.c_char_p, []),
     ("sptb_version", C.c_int32, []),
     ("sptb_launch_count", C.c_int64, []),
+    ("sptb_fft_count", C.c_int64, []),
+    ("sptb_time_spmm", C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int64)]),
     ("sptb_plan_create", C.c_int, [C.POINTER(_P), C.POINTER(Geometry), C.POINTER(Kernel),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double]),
     ("sptb_plan_destroy", C.c_int, [_P]),

@@ -45,66 +45,67 @@ __device__ __forceinline__ void cmac(C& acc, const C& a, const C& b) {
 // ---------------------------------------------------------------------------
 // CSR SpMM over a batch-innermost dense operand.
 //
-// One CTA owns TILE consecutive rows.  A "group" of G lanes computes one row
-// for all BB = G*CPL*CW batch columns (every gathered nonzero is one
-// contiguous BB*sizeof(C) run of x -> 8/16-byte coalesced lane loads).
+// One CTA owns TILE consecutive rows.  The tile's row pointers and, when they
+// fit (<= CAP entries), its column indices and values are staged in shared
+// memory with coalesced loads, so the gather loop issues only the 8/16-byte
+// lane loads of x (one contiguous BB*sizeof(C) run per nonzero) plus FMAs.
+// A "group" of G lanes computes one row for all BB = G*CPL*CW columns.
 // Rows longer than LMAX nonzeros (the skewed centre of S: up to 4852 at
-// 2048^2 x 1536) are split into NCH fixed chunks shared by all groups of the
-// CTA and combined in chunk order, so results are deterministic and do not
-// depend on which group ran which chunk.
+// 2048^2 x 1536) are flagged with a warp ballot and split into NCH fixed
+// chunks shared by all groups of the CTA, combined in chunk order -- results
+// are deterministic and independent of which group ran which chunk.
 // TRANS: the tile is staged in shared memory and written [b][row] (the
-// batch-outer layout cuFFT wants), i.e. the layout transpose is fused into
-// the epilogue.  SUB: y = sub - A x  ([row][b]).
+// batch-outer layout cuFFT wants): the layout transpose is fused into the
+// epilogue.  SUB: y = sub - A x  ([row][b]).
 // ---------------------------------------------------------------------------
 constexpr int SPMM_THREADS = 256;
 constexpr int LMAX = 64;
 constexpr int NCH = 16;
 constexpr int UNR = 8;
+constexpr int CAP = 1024;  // staged nonzeros per tile
 
 template <typename R, int G, int CPL, int CW>
 struct SpmmCfg {
     static constexpr int BB = G * CPL * CW;
     static constexpr int NG = SPMM_THREADS / G;
-    static constexpr int TILE = (4 * NG < 32) ? 32 : 4 * NG;
+    static constexpr int TILE = (4 * NG < 64) ? 64 : (4 * NG > 256 ? 256 : 4 * NG);
 };
 
-template <typename R, int G, int CPL, int CW>
+// acc += sum_k val[k] * x[col[k]]  over k in [beg, end), metadata from smem
+// (STAGED) or global memory; UNR gathers issued before their FMAs.
+template <typename R, int G, int CPL, int CW, bool STAGED>
 __device__ __forceinline__ void row_accumulate(
     const int* __restrict__ ci, const typename Cplx<R>::T* __restrict__ cv,
     const typename Cplx<R>::T* __restrict__ x, int beg, int end, int lig,
     typename Cplx<R>::T (&acc)[CPL][CW]) {
     using C = typename Cplx<R>::T;
     constexpr int BB = G * CPL * CW;
+    const C* xl = x + (size_t)lig * CW;
+    // every chunk issues all of its (predicated) gathers before any FMA, so a
+    // typical row (<= UNR nonzeros) costs one memory round trip
     for (int k = beg; k < end; k += UNR) {
         int cc[UNR];
         C vv[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const int kk = k + u;
-            const bool ok = kk < end;
-            cc[u] = ok ? __ldg(ci + kk) : 0;
+            const bool ok = k + u < end;
+            cc[u] = ok ? (STAGED ? ci[k + u] : __ldg(ci + k + u)) : -1;
             C z;
-            z.x = 0;
-            z.y = 0;
-            vv[u] = ok ? cv[kk] : z;
+            z.x = z.y = 0;
+            vv[u] = ok ? cv[k + u] : z;
         }
         C xs[UNR][CPL][CW];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
+        for (int u = 0; u < UNR; ++u)
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-                if (k + u < end) {
-                    const C* src = x + (size_t)cc[u] * BB + (size_t)(q * G + lig) * CW;
-                    Chunk<R, CW>::ld(src, xs[u][q]);
+                if (cc[u] >= 0) {
+                    Chunk<R, CW>::ld(xl + (size_t)cc[u] * BB + (size_t)q * G * CW, xs[u][q]);
                 } else {
 #pragma unroll
-                    for (int w = 0; w < CW; ++w) {
-                        xs[u][q][w].x = 0;
-                        xs[u][q][w].y = 0;
-                    }
+                    for (int w = 0; w < CW; ++w) xs[u][q][w].x = xs[u][q][w].y = 0;
                 }
             }
-        }
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -124,16 +125,34 @@ k_spmm(const int* __restrict__ rp, const int* __restrict__ ci,
     using Cfg = SpmmCfg<R, G, CPL, CW>;
     constexpr int BB = Cfg::BB, NG = Cfg::NG, TILE = Cfg::TILE;
     constexpr int LD = BB + 1;  // padded smem row (bank spread)
+    constexpr int NW = TILE / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C* part = reinterpret_cast<C*>(smem_raw);  // [NCH][BB]
-    C* tile = part + NCH * BB;                 // [TILE][LD] (TRANS only)
+    C* s_val = reinterpret_cast<C*>(smem_raw);          // [CAP]
+    C* part = s_val + CAP;                              // [NCH][BB]
+    C* tile = part + NCH * BB;                          // [TILE][LD] (TRANS only)
     __shared__ int s_rp[TILE + 1];
+    __shared__ int s_col[CAP];
+    __shared__ unsigned s_long[NW];
 
     const int tid = threadIdx.x;
     const int g = tid / G, lig = tid % G;
     const int row0 = blockIdx.x * TILE;
     const int nrows = min(TILE, rows - row0);
     for (int i = tid; i <= nrows; i += SPMM_THREADS) s_rp[i] = rp[row0 + i];
+    __syncthreads();
+    const int e0 = s_rp[0], ne = s_rp[nrows] - e0;
+    const bool staged = ne <= CAP;
+    if (staged) {
+        for (int i = tid; i < ne; i += SPMM_THREADS) {
+            s_col[i] = __ldg(ci + e0 + i);
+            s_val[i] = cv[e0 + i];
+        }
+    }
+    for (int r = tid; r < NW * 32; r += SPMM_THREADS) {
+        const bool lng = r < nrows && (s_rp[r + 1] - s_rp[r]) > LMAX;
+        const unsigned m = __ballot_sync(0xffffffffu, lng);
+        if ((r & 31) == 0) s_long[r >> 5] = m;
+    }
     __syncthreads();
 
     auto emit = [&](int r, const C (&a)[CPL][CW]) {
@@ -148,7 +167,7 @@ k_spmm(const int* __restrict__ rp, const int* __restrict__ ci,
                     const size_t o = (size_t)(row0 + r) * BB + b;
                     C v = a[q][w];
                     if (SUB) {
-                        C s = sub[o];
+                        const C s = sub[o];
                         v.x = s.x - v.x;
                         v.y = s.y - v.y;
                     }
@@ -159,67 +178,71 @@ k_spmm(const int* __restrict__ rp, const int* __restrict__ ci,
 
     // short rows: one group per row
     for (int r = g; r < nrows; r += NG) {
-        const int beg = s_rp[r], end = s_rp[r + 1];
+        const int beg = s_rp[r] - e0, end = s_rp[r + 1] - e0;
         if (end - beg > LMAX) continue;
         C acc[CPL][CW];
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
 #pragma unroll
-            for (int w = 0; w < CW; ++w) {
-                acc[q][w].x = 0;
-                acc[q][w].y = 0;
-            }
-        row_accumulate<R, G, CPL, CW>(ci, cv, x, beg, end, lig, acc);
+            for (int w = 0; w < CW; ++w) acc[q][w].x = acc[q][w].y = 0;
+        if (staged)
+            row_accumulate<R, G, CPL, CW, true>(s_col, s_val, x, beg, end, lig, acc);
+        else
+            row_accumulate<R, G, CPL, CW, false>(ci + e0, cv + e0, x, beg, end, lig, acc);
         emit(r, acc);
     }
 
-    // long rows: NCH fixed chunks over all groups, combined in chunk order
-    for (int r = 0; r < nrows; ++r) {
-        const int beg = s_rp[r], end = s_rp[r + 1];
-        const int len = end - beg;
-        if (len <= LMAX) continue;
-        for (int c = g; c < NCH; c += NG) {
-            const int cb = beg + (int)(((long long)len * c) / NCH);
-            const int ce = beg + (int)(((long long)len * (c + 1)) / NCH);
-            C acc[CPL][CW];
+    // long rows (ballot mask, ascending): NCH chunks over all groups
+    for (int wd = 0; wd < NW; ++wd) {
+        unsigned m = s_long[wd];
+        while (m) {
+            const int r = wd * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            const int beg = s_rp[r] - e0, len = s_rp[r + 1] - s_rp[r];
+            for (int c = g; c < NCH; c += NG) {
+                const int cb = beg + (int)(((long long)len * c) / NCH);
+                const int ce = beg + (int)(((long long)len * (c + 1)) / NCH);
+                C acc[CPL][CW];
 #pragma unroll
-            for (int q = 0; q < CPL; ++q)
+                for (int q = 0; q < CPL; ++q)
 #pragma unroll
-                for (int w = 0; w < CW; ++w) {
-                    acc[q][w].x = 0;
-                    acc[q][w].y = 0;
-                }
-            row_accumulate<R, G, CPL, CW>(ci, cv, x, cb, ce, lig, acc);
+                    for (int w = 0; w < CW; ++w) acc[q][w].x = acc[q][w].y = 0;
+                if (staged)
+                    row_accumulate<R, G, CPL, CW, true>(s_col, s_val, x, cb, ce, lig, acc);
+                else
+                    row_accumulate<R, G, CPL, CW, false>(ci + e0, cv + e0, x, cb, ce, lig, acc);
 #pragma unroll
-            for (int q = 0; q < CPL; ++q)
+                for (int q = 0; q < CPL; ++q)
 #pragma unroll
-                for (int w = 0; w < CW; ++w) part[c * BB + (q * G + lig) * CW + w] = acc[q][w];
-        }
-        __syncthreads();
-        for (int b = tid; b < BB; b += SPMM_THREADS) {
-            C s = part[b];
-            for (int c = 1; c < NCH; ++c) {
-                s.x += part[c * BB + b].x;
-                s.y += part[c * BB + b].y;
+                    for (int w = 0; w < CW; ++w) part[c * BB + (q * G + lig) * CW + w] = acc[q][w];
             }
-            if (TRANS) {
-                tile[r * LD + b] = s;
-            } else {
-                const size_t o = (size_t)(row0 + r) * BB + b;
-                if (SUB) {
-                    C t = sub[o];
-                    s.x = t.x - s.x;
-                    s.y = t.y - s.y;
+            __syncthreads();
+            for (int b = tid; b < BB; b += SPMM_THREADS) {
+                C s = part[b];
+                for (int c = 1; c < NCH; ++c) {
+                    s.x += part[c * BB + b].x;
+                    s.y += part[c * BB + b].y;
                 }
-                y[o] = s;
+                if (TRANS) {
+                    tile[r * LD + b] = s;
+                } else {
+                    const size_t o = (size_t)(row0 + r) * BB + b;
+                    if (SUB) {
+                        const C t = sub[o];
+                        s.x = t.x - s.x;
+                        s.y = t.y - s.y;
+                    }
+                    y[o] = s;
+                }
             }
+            __syncthreads();
         }
-        __syncthreads();
     }
 
     if (TRANS) {
         __syncthreads();
         // y[b][row0 + i]: consecutive threads -> consecutive rows
+#pragma unroll 4
         for (int e = tid; e < BB * TILE; e += SPMM_THREADS) {
             const int b = e / TILE, i = e % TILE;
             if (i < nrows) y[(size_t)b * rows + row0 + i] = tile[i * LD + b];
@@ -235,10 +258,10 @@ static int spmm_dispatch(const DevCSR& A, const void* val, const void* x, void* 
     const int rows = (int)A.rows;
     if (rows == 0) return SPTB_OK;
     const int grid = (rows + Cfg::TILE - 1) / Cfg::TILE;
-    size_t sm = (size_t)NCH * Cfg::BB * sizeof(C);
+    size_t sm = (size_t)(CAP + NCH * Cfg::BB) * sizeof(C);
     if (trans) sm += (size_t)Cfg::TILE * (Cfg::BB + 1) * sizeof(C);
     auto run = [&](auto kern) -> int {
-        if (sm > 48 * 1024) SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         kern<<<grid, SPMM_THREADS, sm, st>>>(A.row_ptr, A.col, (const C*)val, (const C*)x,
                                              (C*)y, (const C*)sub, rows);
         SPTB_LAUNCHED();
@@ -318,62 +341,97 @@ template int launch_transpose_bm_to_mb<double>(const void*, void*, int, int64_t,
 // ---------------------------------------------------------------------------
 // pack / unpack between caller slices and complex [b][len]
 // (pairing a + ib of slices (2k, 2k+1): pipeline.py:122-159)
+// gridDim = (nblk, B): block-uniform unit b, each thread handles 4 elements
+// of the plane with independent loads issued before any store.
 // ---------------------------------------------------------------------------
+constexpr int PK = 4;
+
 template <typename TI, typename R>
-__global__ void k_pack(const TI* __restrict__ in, bool cplx, long long n, long long u0, int nb,
-                       long long len, const R* __restrict__ plane,
-                       typename Cplx<R>::T* __restrict__ out, int B) {
+__global__ void __launch_bounds__(256)
+k_pack(const TI* __restrict__ in, bool cplx, long long n, long long u0, int nb, long long len,
+       const R* __restrict__ plane, typename Cplx<R>::T* __restrict__ out) {
     using C = typename Cplx<R>::T;
-    const long long total = (long long)B * len;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int b = (int)(e / len);
-        const long long i = e - (long long)b * len;
-        C v;
-        v.x = 0;
-        v.y = 0;
-        if (b < nb) {
-            const long long u = u0 + b;
-            R re, im;
-            if (cplx) {
-                re = (R)in[(u * len + i) * 2];
-                im = (R)in[(u * len + i) * 2 + 1];
-            } else {
-                re = (R)in[(2 * u) * len + i];
-                im = (2 * u + 1 < n) ? (R)in[(2 * u + 1) * len + i] : (R)0;
-            }
-            if (plane) {
-                const R d = plane[i];
-                re *= d;
-                im *= d;
-            }
-            v.x = re;
-            v.y = im;
+    const int b = blockIdx.y;
+    C* dst = out + (size_t)b * len;
+    const long long u = u0 + b;
+    const TI* pa = nullptr;
+    const TI* pb = nullptr;
+    long long es = 1;
+    if (b < nb) {
+        if (cplx) {
+            pa = in + u * len * 2;
+            pb = pa + 1;
+            es = 2;
+        } else {
+            pa = in + (2 * u) * len;
+            pb = (2 * u + 1 < n) ? in + (2 * u + 1) * len : nullptr;
         }
-        out[e] = v;
+    }
+    const long long stride = (long long)gridDim.x * blockDim.x * PK;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * PK + threadIdx.x; i0 < len; i0 += stride) {
+        R re[PK], im[PK], d[PK];
+#pragma unroll
+        for (int k = 0; k < PK; ++k) {
+            const long long i = i0 + (long long)k * blockDim.x;
+            re[k] = im[k] = (R)0;
+            d[k] = (R)1;
+            if (i < len && pa) {
+                re[k] = (R)pa[i * es];
+                if (pb) im[k] = (R)pb[i * es];
+                if (plane) d[k] = plane[i];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PK; ++k) {
+            const long long i = i0 + (long long)k * blockDim.x;
+            if (i < len) {
+                C v;
+                v.x = re[k] * d[k];
+                v.y = im[k] * d[k];
+                dst[i] = v;
+            }
+        }
     }
 }
 
 template <typename TO, typename R>
-__global__ void k_unpack(const typename Cplx<R>::T* __restrict__ z, long long len,
-                         const R* __restrict__ plane, R scale, TO* __restrict__ out, bool cplx,
-                         long long n, long long u0, int nb) {
-    const long long total = (long long)nb * len;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int b = (int)(e / len);
-        const long long i = e - (long long)b * len;
-        const long long u = u0 + b;
-        R f = scale;
-        if (plane) f *= plane[i];
-        const auto v = z[e];
-        const R re = v.x * f, im = v.y * f;
-        if (cplx) {
-            out[(u * len + i) * 2] = (TO)re;
-            out[(u * len + i) * 2 + 1] = (TO)im;
-        } else {
-            out[(2 * u) * len + i] = (TO)re;
-            if (2 * u + 1 < n) out[(2 * u + 1) * len + i] = (TO)im;
+__global__ void __launch_bounds__(256)
+k_unpack(const typename Cplx<R>::T* __restrict__ z, long long len, const R* __restrict__ plane,
+         R scale, TO* __restrict__ out, bool cplx, long long n, long long u0) {
+    using C = typename Cplx<R>::T;
+    const int b = blockIdx.y;
+    const C* src = z + (size_t)b * len;
+    const long long u = u0 + b;
+    TO* pa;
+    TO* pb;
+    long long es = 1;
+    if (cplx) {
+        pa = out + u * len * 2;
+        pb = pa + 1;
+        es = 2;
+    } else {
+        pa = out + (2 * u) * len;
+        pb = (2 * u + 1 < n) ? out + (2 * u + 1) * len : nullptr;
+    }
+    const long long stride = (long long)gridDim.x * blockDim.x * PK;
+    for (long long i0 = (long long)blockIdx.x * blockDim.x * PK + threadIdx.x; i0 < len; i0 += stride) {
+        C v[PK];
+        R f[PK];
+#pragma unroll
+        for (int k = 0; k < PK; ++k) {
+            const long long i = i0 + (long long)k * blockDim.x;
+            if (i < len) {
+                v[k] = src[i];
+                f[k] = plane ? plane[i] * scale : scale;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PK; ++k) {
+            const long long i = i0 + (long long)k * blockDim.x;
+            if (i < len) {
+                pa[i * es] = (TO)(v[k].x * f[k]);
+                if (pb) pb[i * es] = (TO)(v[k].y * f[k]);
+            }
         }
     }
 }
@@ -383,18 +441,25 @@ static int grid_for(long long total) {
     return (int)std::min<long long>(g, 148LL * 32);
 }
 
+static dim3 plane_grid(long long len, int nplanes) {
+    long long per = (len + 256LL * PK - 1) / (256LL * PK);
+    const long long cap = std::max<long long>(1, 148LL * 16 / std::max(1, nplanes));
+    return dim3((unsigned)std::max<long long>(1, std::min(per, std::max<long long>(cap, 1))),
+                (unsigned)nplanes);
+}
+
 template <typename R>
 int launch_pack(const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, int64_t len,
                 const void* plane, void* out, cudaStream_t st) {
     using C = typename Cplx<R>::T;
     const bool cplx = fmt & SPTB_FMT_COMPLEX;
-    const int grid = grid_for((long long)B * len);
+    const dim3 grid = plane_grid(len, B);
     if (fmt & SPTB_FMT_F64)
         k_pack<double, R><<<grid, 256, 0, st>>>((const double*)in, cplx, n, u0, nb, len,
-                                                (const R*)plane, (C*)out, B);
+                                                (const R*)plane, (C*)out);
     else
         k_pack<float, R><<<grid, 256, 0, st>>>((const float*)in, cplx, n, u0, nb, len,
-                                               (const R*)plane, (C*)out, B);
+                                               (const R*)plane, (C*)out);
     SPTB_LAUNCHED();
     return SPTB_OK;
 }
@@ -406,13 +471,13 @@ int launch_unpack(const void* in, int64_t len, const void* plane, double scale, 
                   int fmt, int64_t n, int64_t u0, int nb, cudaStream_t st) {
     using C = typename Cplx<R>::T;
     const bool cplx = fmt & SPTB_FMT_COMPLEX;
-    const int grid = grid_for((long long)nb * len);
+    const dim3 grid = plane_grid(len, nb);
     if (fmt & SPTB_FMT_F64)
         k_unpack<double, R><<<grid, 256, 0, st>>>((const C*)in, len, (const R*)plane, (R)scale,
-                                                  (double*)out, cplx, n, u0, nb);
+                                                  (double*)out, cplx, n, u0);
     else
         k_unpack<float, R><<<grid, 256, 0, st>>>((const C*)in, len, (const R*)plane, (R)scale,
-                                                 (float*)out, cplx, n, u0, nb);
+                                                 (float*)out, cplx, n, u0);
     SPTB_LAUNCHED();
     return SPTB_OK;
 }

@@ -11,6 +11,8 @@ namespace sptb {
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_ffts{0};
+void count_fft(int n) { g_ffts += n; }
 
 void set_error(const std::string& m) { g_err = m; }
 int fail(int code, const std::string& m) {
@@ -85,7 +87,7 @@ int get_fft(sptb_plan* p, int B, FFTPlans** out) {
 }
 
 static int exec_fft(sptb_plan* p, cufftHandle h, void* z, int dir) {
-    count_launch();
+    count_fft();
     if (p->prec == SPTB_PREC_F64)
         SPTB_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)z, (cufftDoubleComplex*)z, dir));
     else
@@ -255,6 +257,7 @@ extern "C" {
 const char* sptb_last_error(void) { return g_err.c_str(); }
 int32_t sptb_version(void) { return 1; }
 int64_t sptb_launch_count(void) { return g_launches.load(); }
+int64_t sptb_fft_count(void) { return g_ffts.load(); }
 
 int sptb_plan_create(sptb_plan** out, const sptb_geometry* g, const sptb_kernel* k,
                      int32_t precision, int32_t max_batch, int32_t device, double threshold) {
@@ -306,7 +309,9 @@ int sptb_plan_destroy(sptb_plan* p) {
     }
     void* bufs[] = {p->S.row_ptr, p->S.col, p->S.val, p->SH.row_ptr, p->SH.col, p->SH.val,
                     p->SW_val, p->w_dev, p->deapo, p->G0, p->G1, p->G2, p->S0, p->S1,
-                    p->stage_in, p->stage_out, p->red, p->fft_work};
+                    p->stage_in, p->stage_out, p->red, p->fft_work,
+                    p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
+                    p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->extra)

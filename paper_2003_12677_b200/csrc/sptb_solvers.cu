@@ -85,18 +85,23 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[K], double* out
     }
 }
 
-// partial[(blk*B + b)*K + k] -> sums[b*K + k], fixed order over blk
+// partial[(blk*B + b)*K + k] -> sums[b*K + k]: one warp per output, lanes take
+// blk = lane, lane+32, ... and a fixed shuffle tree combines them (deterministic)
 __global__ void k_finish(const double* __restrict__ part, int nblk, int B, int K, int is_max,
                          double* __restrict__ sums) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * K) return;
-    const int b = i / K, k = i % K;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= B * K) return;
+    const int b = w / K, k = w % K;
     double s = 0;
-    for (int blk = 0; blk < nblk; ++blk) {
+    for (int blk = lane; blk < nblk; blk += 32) {
         const double v = part[((size_t)blk * B + b) * K + k];
         s = is_max ? fmax(s, v) : s + v;
     }
-    sums[i] = s;
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_down_sync(0xffffffffu, s, o);
+        s = is_max ? fmax(s, t) : s + t;
+    }
+    if (lane == 0) sums[w] = s;
 }
 
 // grid kernels: gridDim = (nblk, B); block-uniform unit b; element (b, m)
@@ -111,9 +116,22 @@ __global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
 #pragma unroll
     for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0;
     if (op.enabled(b)) {
-        const long long stride = (long long)gridDim.x * RT;
-        for (long long m = blockIdx.x * (long long)RT + threadIdx.x; m < M; m += stride)
-            op(b, (size_t)b * M + m, m, acc);
+        constexpr int U = 4;
+        using In = typename Op::In;
+        const long long stride = (long long)gridDim.x * RT * U;
+        for (long long m0 = blockIdx.x * (long long)RT * U + threadIdx.x; m0 < M; m0 += stride) {
+            In v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long m = m0 + (long long)u * RT;
+                if (m < M) v[u] = op.load(b, (size_t)b * M + m, m);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long m = m0 + (long long)u * RT;
+                if (m < M) op.apply(b, (size_t)b * M + m, m, v[u], acc);
+            }
+        }
     }
     if constexpr (K > 0) block_reduce_store<K, MAX>(acc, part + ((size_t)blockIdx.x * gridDim.y + b) * K);
 }
@@ -164,7 +182,12 @@ __device__ __forceinline__ D2 grad_t(const D2* vx, const D2* vy, size_t i, long 
     return make_double2(-re, -im);
 }
 
-// ------------------------------------------------------------------ grid ops (SIRT / FBP)
+// ------------------------------------------------------------------ grid ops
+// Two-phase element ops: load() gathers every input of element i (and its
+// stencil neighbours) into registers, apply() computes, stores and
+// accumulates.  k_grid issues the loads of U elements before any store, so
+// the (always element-local) read-write pairs cannot serialise the loop on
+// memory latency through conservative aliasing.
 
 template <typename R>
 struct OpSirtUpdate {  // u += alpha g; [nonneg]; W = deapo u; count non-finite u
@@ -175,14 +198,21 @@ struct OpSirtUpdate {  // u += alpha g; [nonneg]; W = deapo u; count non-finite 
     const R* deapo;
     const Unit* us;
     int nonneg;
+    struct In { C x, g; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
-        C x = u[i];
+    __device__ In load(int b, size_t i, long long m) const {
+        In v;
+        v.x = u[i];
+        v.g = us[b].active ? g[i] : C{};
+        v.d = deapo[m];
+        return v;
+    }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
+        C x = v.x;
         const Unit& un = us[b];
         if (un.active) {
-            const C gg = g[i];
-            x.x = (R)((double)x.x + un.alpha[0] * (double)gg.x);
-            x.y = (R)((double)x.y + un.alpha[1] * (double)gg.y);
+            x.x = (R)((double)x.x + un.alpha[0] * (double)v.g.x);
+            x.y = (R)((double)x.y + un.alpha[1] * (double)v.g.y);
             if (nonneg) {
                 x.x = pos_(x.x);
                 x.y = pos_(x.y);
@@ -190,8 +220,7 @@ struct OpSirtUpdate {  // u += alpha g; [nonneg]; W = deapo u; count non-finite 
             u[i] = x;
         }
         if (!finite2(x.x, x.y)) acc[0] += 1.0;
-        const R d = deapo[m];
-        w[i] = rc<R>(x.x * d, x.y * d);
+        w[i] = rc<R>(x.x * v.d, x.y * v.d);
     }
 };
 
@@ -202,11 +231,12 @@ struct OpDeapo {  // w = deapo * v * scale  (v of any precision, w of plan preci
     C* w;
     const R* deapo;
     double scale;
+    struct In { V x; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
-        const D2 x = d2(v[i]);
-        const double d = (double)deapo[m] * scale;
-        w[i] = rc<R>(x.x * d, x.y * d);
+    __device__ In load(int, size_t i, long long m) const { return In{v[i], deapo[m]}; }
+    __device__ void apply(int, size_t i, long long, const In& q, double (&)[1]) const {
+        const double d = (double)q.d * scale;
+        w[i] = rc<R>(q.x.x * d, q.x.y * d);
     }
 };
 
@@ -217,13 +247,14 @@ struct OpStore {  // out = deapo * y * scale  (V precision)
     V* out;
     const R* deapo;
     double scale;
+    struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
-        const C yy = y[i];
-        const double d = (double)deapo[m] * scale;
+    __device__ In load(int, size_t i, long long m) const { return In{y[i], deapo[m]}; }
+    __device__ void apply(int, size_t i, long long, const In& q, double (&)[1]) const {
+        const double d = (double)q.d * scale;
         V o;
-        o.x = yy.x * d;
-        o.y = yy.y * d;
+        o.x = q.y.x * d;
+        o.y = q.y.y * d;
         out[i] = o;
     }
 };
@@ -237,17 +268,23 @@ struct OpAdjPost {
     C* g;
     const R* deapo;
     double scale;
+    struct In { C y, go; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&acc)[BB ? 4 : 2]) const {
-        const C yy = y[i];
-        const double d = (double)deapo[m] * scale;
-        const C gn = rc<R>(yy.x * d, yy.y * d);
+    __device__ In load(int, size_t i, long long m) const {
+        In v;
+        v.y = y[i];
+        v.go = BB ? g[i] : C{};
+        v.d = deapo[m];
+        return v;
+    }
+    __device__ void apply(int, size_t i, long long, const In& v, double (&acc)[BB ? 4 : 2]) const {
+        const double d = (double)v.d * scale;
+        const C gn = rc<R>(v.y.x * d, v.y.y * d);
         if (BB) {
-            const C go = g[i];
-            acc[0] += (double)go.x * go.x;
-            acc[1] += (double)go.y * go.y;
-            acc[2] += (double)go.x * ((double)go.x - (double)gn.x);
-            acc[3] += (double)go.y * ((double)go.y - (double)gn.y);
+            acc[0] += (double)v.go.x * v.go.x;
+            acc[1] += (double)v.go.y * v.go.y;
+            acc[2] += (double)v.go.x * ((double)v.go.x - (double)gn.x);
+            acc[3] += (double)v.go.y * ((double)v.go.y - (double)gn.y);
         } else {
             acc[0] += (double)gn.x * gn.x;
             acc[1] += (double)gn.y * gn.y;
@@ -259,10 +296,11 @@ struct OpAdjPost {
 template <typename V>
 struct OpNonfinite {
     const V* u;
+    struct In { V x; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long, double (&acc)[1]) const {
-        const D2 x = d2(u[i]);
-        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+    __device__ In load(int, size_t i, long long) const { return In{u[i]}; }
+    __device__ void apply(int, size_t, long long, const In& v, double (&acc)[1]) const {
+        if (!finite2(v.x.x, v.x.y)) acc[0] += 1.0;
     }
 };
 
@@ -270,9 +308,11 @@ template <typename V>
 struct OpNonneg {
     V* u;
     const Unit* us;
+    struct In { V x; };
     __device__ bool enabled(int b) const { return us[b].status != ST_PAD; }
-    __device__ void operator()(int, size_t i, long long, double (&)[1]) const {
-        V x = u[i];
+    __device__ In load(int, size_t i, long long) const { return In{u[i]}; }
+    __device__ void apply(int, size_t i, long long, const In& v, double (&)[1]) const {
+        V x = v.x;
         x.x = pos_(x.x);
         x.y = pos_(x.y);
         u[i] = x;
@@ -285,12 +325,13 @@ struct OpAbsMax {  // per-channel max |deapo*y*scale| (TV default mu, solvers.py
     const C* y;
     const R* deapo;
     double scale;
+    struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
-        const C yy = y[i];
-        const double d = (double)deapo[m] * scale;
-        acc[0] = fmax(acc[0], fabs((double)(R)(yy.x * d)));
-        acc[1] = fmax(acc[1], fabs((double)(R)(yy.y * d)));
+    __device__ In load(int, size_t i, long long m) const { return In{y[i], deapo[m]}; }
+    __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
+        const double d = (double)v.d * scale;
+        acc[0] = fmax(acc[0], fabs((double)(R)(v.y.x * d)));
+        acc[1] = fmax(acc[1], fabs((double)(R)(v.y.y * d)));
     }
 };
 
@@ -303,11 +344,12 @@ struct OpCglsInit {  // p = s = deapo*y*scale ; <s,s> ; W = deapo p
     D2* p;
     const R* deapo;
     double scale;
+    struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
-        const C yy = w[i];
-        const double d = (double)deapo[m];
-        const D2 s = make_double2(yy.x * d * scale, yy.y * d * scale);
+    __device__ In load(int, size_t i, long long m) const { return In{w[i], deapo[m]}; }
+    __device__ void apply(int, size_t i, long long, const In& v, double (&acc)[2]) const {
+        const double d = (double)v.d;
+        const D2 s = make_double2(v.y.x * d * scale, v.y.y * d * scale);
         acc[0] += s.x * s.x;
         acc[1] += s.y * s.y;
         p[i] = s;
@@ -321,11 +363,12 @@ struct OpDotS {  // <s,s>, s = deapo*y*scale
     const C* y;
     const R* deapo;
     double scale;
+    struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
-        const C yy = y[i];
-        const double d = (double)deapo[m] * scale;
-        const double sx = yy.x * d, sy = yy.y * d;
+    __device__ In load(int, size_t i, long long m) const { return In{y[i], deapo[m]}; }
+    __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
+        const double d = (double)v.d * scale;
+        const double sx = v.y.x * d, sy = v.y.y * d;
         acc[0] += sx * sx;
         acc[1] += sy * sy;
     }
@@ -340,20 +383,21 @@ struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-fi
     const R* deapo;
     double scale;
     const Unit* us;
+    struct In { D2 x, pp; C y; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
+    __device__ In load(int, size_t i, long long m) const { return In{u[i], p[i], w[i], deapo[m]}; }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
         const Unit& un = us[b];
-        D2 x = u[i];
-        D2 pp = p[i];
-        const double d = (double)deapo[m];
+        D2 x = v.x;
+        D2 pp = v.pp;
+        const double d = (double)v.d;
         if (un.stepped) {
             x.x += un.alpha[0] * pp.x;
             x.y += un.alpha[1] * pp.y;
             u[i] = x;
             if (un.active) {
-                const C yy = w[i];
-                pp.x = yy.x * d * scale + un.beta[0] * pp.x;
-                pp.y = yy.y * d * scale + un.beta[1] * pp.y;
+                pp.x = v.y.x * d * scale + un.beta[0] * pp.x;
+                pp.y = v.y.y * d * scale + un.beta[1] * pp.y;
                 p[i] = pp;
             }
         }
@@ -369,11 +413,14 @@ struct OpTvRho {
     const D2 *u, *dx, *dy, *bx, *by;
     D2 *rx, *ry;
     int X, Y;
+    struct In { D2 gx, gy, dx, dy, bx, by; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int, size_t i, long long m, double (&)[1]) const {
-        const D2 gx = grad_x(u, i, m, X), gy = grad_y(u, i, m, X, Y);
-        rx[i] = make_double2(dx[i].x - bx[i].x - gx.x, dx[i].y - bx[i].y - gx.y);
-        ry[i] = make_double2(dy[i].x - by[i].x - gy.x, dy[i].y - by[i].y - gy.y);
+    __device__ In load(int, size_t i, long long m) const {
+        return In{grad_x(u, i, m, X), grad_y(u, i, m, X, Y), dx[i], dy[i], bx[i], by[i]};
+    }
+    __device__ void apply(int, size_t i, long long, const In& v, double (&)[1]) const {
+        rx[i] = make_double2(v.dx.x - v.bx.x - v.gx.x, v.dx.y - v.bx.y - v.gx.y);
+        ry[i] = make_double2(v.dy.x - v.by.x - v.gy.x, v.dy.y - v.by.y - v.gy.y);
     }
 };
 
@@ -389,14 +436,21 @@ struct OpTvS {
     double scale;
     const Unit* us;
     int X, Y;
+    struct In { C y; D2 gt, pp; R d; };
     __device__ bool enabled(int b) const { return MODE == 1 || us[b].active; }
-    __device__ void operator()(int b, size_t i, long long m, double (&acc)[2]) const {
+    __device__ In load(int, size_t i, long long m) const {
+        In v;
+        v.y = w[i];
+        v.gt = grad_t(rx, ry, i, m, X, Y);
+        v.pp = MODE == 2 ? p[i] : D2{};
+        v.d = deapo[m];
+        return v;
+    }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         const Unit& un = us[b];
-        const C yy = w[i];
-        const double d = (double)deapo[m];
-        const D2 gt = grad_t(rx, ry, i, m, X, Y);
-        const D2 s = make_double2(un.mu[0] * (yy.x * d * scale) + un.lam[0] * gt.x,
-                                  un.mu[1] * (yy.y * d * scale) + un.lam[1] * gt.y);
+        const double d = (double)v.d;
+        const D2 s = make_double2(un.mu[0] * (v.y.x * d * scale) + un.lam[0] * v.gt.x,
+                                  un.mu[1] * (v.y.y * d * scale) + un.lam[1] * v.gt.y);
         if (MODE <= 1) {
             acc[0] += s.x * s.x;
             acc[1] += s.y * s.y;
@@ -406,7 +460,7 @@ struct OpTvS {
             w[i] = rc<R>(s.x * d, s.y * d);
         }
         if (MODE == 2) {
-            D2 pp = p[i];
+            D2 pp = v.pp;
             if (!un.inner_stop) {
                 pp.x = s.x + un.beta[0] * pp.x;
                 pp.y = s.y + un.beta[1] * pp.y;
@@ -421,11 +475,14 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     const D2* p;
     const Unit* us;
     int X, Y;
+    struct In { D2 gx, gy; };
     __device__ bool enabled(int b) const { return us[b].active; }
-    __device__ void operator()(int, size_t i, long long m, double (&acc)[2]) const {
-        const D2 gx = grad_x(p, i, m, X), gy = grad_y(p, i, m, X, Y);
-        acc[0] += gx.x * gx.x + gy.x * gy.x;
-        acc[1] += gx.y * gx.y + gy.y * gy.y;
+    __device__ In load(int, size_t i, long long m) const {
+        return In{grad_x(p, i, m, X), grad_y(p, i, m, X, Y)};
+    }
+    __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
+        acc[0] += v.gx.x * v.gx.x + v.gy.x * v.gy.x;
+        acc[1] += v.gx.y * v.gx.y + v.gy.y * v.gy.y;
     }
 };
 
@@ -434,20 +491,21 @@ struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
     const D2* p;
     const Unit* us;
     int X, Y;
+    struct In { D2 pp, gx, gy, x, a, c; };
     __device__ bool enabled(int b) const { return us[b].stepped; }
-    __device__ void operator()(int b, size_t i, long long m, double (&)[1]) const {
+    __device__ In load(int, size_t i, long long m) const {
+        return In{p[i], grad_x(p, i, m, X), grad_y(p, i, m, X, Y), u[i], rx[i], ry[i]};
+    }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
         const Unit& un = us[b];
-        const D2 pp = p[i];
-        const D2 gx = grad_x(p, i, m, X), gy = grad_y(p, i, m, X, Y);
-        D2 x = u[i];
-        x.x += un.alpha[0] * pp.x;
-        x.y += un.alpha[1] * pp.y;
+        D2 x = v.x, a = v.a, c = v.c;
+        x.x += un.alpha[0] * v.pp.x;
+        x.y += un.alpha[1] * v.pp.y;
+        a.x -= un.alpha[0] * v.gx.x;
+        a.y -= un.alpha[1] * v.gx.y;
+        c.x -= un.alpha[0] * v.gy.x;
+        c.y -= un.alpha[1] * v.gy.y;
         u[i] = x;
-        D2 a = rx[i], c = ry[i];
-        a.x -= un.alpha[0] * gx.x;
-        a.y -= un.alpha[1] * gx.y;
-        c.x -= un.alpha[0] * gy.x;
-        c.y -= un.alpha[1] * gy.y;
         rx[i] = a;
         ry[i] = c;
     }
@@ -463,18 +521,19 @@ struct OpTvShrink {
     const R* deapo;
     const Unit* us;
     int X, Y;
+    struct In { D2 x, gx, gy, bx, by; R d; };
     __device__ bool enabled(int) const { return true; }
-    __device__ void operator()(int b, size_t i, long long m, double (&acc)[1]) const {
+    __device__ In load(int, size_t i, long long m) const {
+        return In{u[i], grad_x(u, i, m, X), grad_y(u, i, m, X, Y), bx[i], by[i], deapo[m]};
+    }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
         const Unit& un = us[b];
-        const D2 x = u[i];
-        if (!finite2(x.x, x.y)) acc[0] += 1.0;
-        const double d = (double)deapo[m];
-        w[i] = rc<R>(x.x * d, x.y * d);
+        if (!finite2(v.x.x, v.x.y)) acc[0] += 1.0;
+        const double d = (double)v.d;
+        w[i] = rc<R>(v.x.x * d, v.x.y * d);
         if (!un.active) return;
-        const D2 gx = grad_x(u, i, m, X), gy = grad_y(u, i, m, X, Y);
-        const D2 vbx = bx[i], vby = by[i];
-        const double vx[2] = {gx.x + vbx.x, gx.y + vbx.y};
-        const double vy[2] = {gy.x + vby.x, gy.y + vby.y};
+        const double vx[2] = {v.gx.x + v.bx.x, v.gx.y + v.bx.y};
+        const double vy[2] = {v.gy.x + v.by.x, v.gy.y + v.by.y};
         double ox[2], oy[2];
         for (int c = 0; c < 2; ++c) {
             const double kap = 1.0 / un.lam[c];
@@ -485,8 +544,8 @@ struct OpTvShrink {
         }
         dx[i] = make_double2(ox[0], ox[1]);
         dy[i] = make_double2(oy[0], oy[1]);
-        bx[i] = make_double2(vbx.x + gx.x - ox[0], vbx.y + gx.y - ox[1]);
-        by[i] = make_double2(vby.x + gy.x - oy[0], vby.y + gy.y - oy[1]);
+        bx[i] = make_double2(v.bx.x + v.gx.x - ox[0], v.bx.y + v.gx.y - ox[1]);
+        by[i] = make_double2(v.by.x + v.gy.x - oy[0], v.by.y + v.gy.y - oy[1]);
     }
 };
 
@@ -511,9 +570,14 @@ k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
         ap = 0.5 * (us[b].alpha[0] + us[b].alpha[1]);
         am = 0.5 * (us[b].alpha[0] - us[b].alpha[1]);
     }
-    for (long long idx = blockIdx.x * (long long)RT + threadIdx.x; idx < total; idx += stride) {
-        const long long q = idx / B;
-        const int t = (int)(q / H), jh = (int)(q % H);
+    // blocks walk whole detector rows t; inside a row (jh, b) in 32-bit math
+    // (B is a power of two: the divide is a shift)
+    (void)total;
+    (void)stride;
+    const int per_row = H * B;
+    for (int t = blockIdx.x; t < T; t += gridDim.x)
+    for (int e = threadIdx.x; e < per_row; e += RT) {
+        const int jh = e / B;
         const int j1 = jh, j2 = (P - jh) % P;
         if (j1 > j2 && j2 != 0) continue;  // odd P: each pair once
         const size_t s1 = (size_t)t * P + j1, s2 = (size_t)t * P + j2;
@@ -936,7 +1000,7 @@ struct Solver {
         k_grid<K, MAX, Op><<<g, RT, 0, st>>>(op, p->M, part);
         SPTB_LAUNCHED();
         if (K > 0 && out_sums) {
-            k_finish<<<(B * K + 127) / 128, 128, 0, st>>>(part, nblk_grid, B, K, MAX ? 1 : 0,
+            k_finish<<<(B * K * 32 + 255) / 256, 256, 0, st>>>(part, nblk_grid, B, K, MAX ? 1 : 0,
                                                           out_sums);
             SPTB_LAUNCHED();
         }
@@ -948,13 +1012,13 @@ struct Solver {
         k_spec<R, RV, UPDATE><<<nblk_spec, RT, 0, st>>>(rh, qh, rf, (const R*)p->w_dev, p->w_len,
                                                         p->T, p->P, B, us, part);
         SPTB_LAUNCHED();
-        k_finish<<<(B * 2 + 127) / 128, 128, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
+        k_finish<<<(B * 2 * 32 + 255) / 256, 256, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
         SPTB_LAUNCHED();
         return SPTB_OK;
     }
 
     int fft(cufftHandle h, void* z, int dir) {
-        count_launch();
+        count_fft();
         if (sizeof(R) == 8)
             SPTB_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)z, (cufftDoubleComplex*)z, dir));
         else

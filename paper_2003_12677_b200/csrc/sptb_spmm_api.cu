@@ -3,6 +3,7 @@
 #include "sptb_internal.cuh"
 
 #include <algorithm>
+#include <vector>
 
 namespace sptb {
 
@@ -130,4 +131,72 @@ extern "C" int sptb_spmm(sptb_plan* p, int32_t which, const void* x, void* y, in
     cudaSetDevice(p->device);
     return p->prec == SPTB_PREC_F64 ? spmm_ref<double>(p, which, x, y, nrhs, fmt)
                                     : spmm_ref<float>(p, which, x, y, nrhs, fmt);
+}
+
+// ---------------------------------------------------------------- benchmark hook
+namespace sptb {
+
+template <typename C>
+__global__ void k_fill_pattern(C* x, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned h = (unsigned)(i * 2654435761u);
+        C v;
+        v.x = (float)((h & 0xffff) * (1.0 / 65536.0) - 0.5);
+        v.y = (float)((h >> 16) * (1.0 / 65536.0) - 0.5);
+        x[i] = v;
+    }
+}
+
+template <typename R>
+int time_spmm(sptb_plan* p, int which, int B, int reps, double* ms) {
+    using C = typename CplxT<R>::T;
+    const DevCSR& A = (which == SPTB_MAT_SH) ? p->SH : p->S;
+    const void* vals = A.val;
+    if (which == SPTB_MAT_SW) {
+        if (!p->SW_val) return fail(SPTB_ERR_STATE, "no filter set");
+        vals = p->SW_val;
+    }
+    SPTB_TRY(ensure_work(p, B));
+    C* x = (C*)(which == SPTB_MAT_SH ? p->G1 : p->S1);
+    C* y = (C*)(which == SPTB_MAT_SH ? p->S0 : p->G0);
+    const long long nx = (long long)B * A.cols;
+    k_fill_pattern<C><<<gridn(nx), 256, 0, p->stream>>>(x, nx);
+    SPTB_LAUNCHED();
+    for (int w = 0; w < 2; ++w) SPTB_TRY(launch_spmm<R>(A, vals, x, y, B, true, nullptr, p->stream));
+    cudaEvent_t e0, e1;
+    SPTB_CUDA(cudaEventCreate(&e0));
+    SPTB_CUDA(cudaEventCreate(&e1));
+    SPTB_CUDA(cudaEventRecord(e0, p->stream));
+    for (int r = 0; r < reps; ++r)
+        SPTB_TRY(launch_spmm<R>(A, vals, x, y, B, true, nullptr, p->stream));
+    SPTB_CUDA(cudaEventRecord(e1, p->stream));
+    SPTB_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    SPTB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = (double)t / reps;
+    return SPTB_OK;
+}
+
+}  // namespace sptb
+
+extern "C" int sptb_time_spmm(sptb_plan* p, int32_t which, int32_t B, int32_t reps,
+                              double* ms_per_launch, int64_t* distinct_inputs) {
+    if (!p || !ms_per_launch) return fail(SPTB_ERR_ARG, "null argument");
+    if (B < 1 || B > 64 || (B & (B - 1))) return fail(SPTB_ERR_ARG, "B must be a power of two <= 64");
+    if (reps < 1) return fail(SPTB_ERR_ARG, "reps must be >= 1");
+    cudaSetDevice(p->device);
+    if (distinct_inputs) {
+        // input rows of S are samples (rows of S^H) and vice versa: count non-empty ones
+        const DevCSR& other = (which == SPTB_MAT_SH) ? p->S : p->SH;
+        std::vector<int> rp(other.rows + 1);
+        SPTB_CUDA(cudaMemcpy(rp.data(), other.row_ptr, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost));
+        int64_t c = 0;
+        for (int64_t i = 0; i < other.rows; ++i) c += rp[i + 1] > rp[i];
+        *distinct_inputs = c;
+    }
+    return p->prec == SPTB_PREC_F64 ? time_spmm<double>(p, which, B, reps, ms_per_launch)
+                                    : time_spmm<float>(p, which, B, reps, ms_per_launch);
 }
