@@ -638,9 +638,11 @@ __global__ void k_convert(const A* __restrict__ src, Bt* __restrict__ dst, long 
 
 // ------------------------------------------------------------------ scalar kernels
 // A, C -> per-channel squared weighted norms
+// (clamps rounding negatives to 0 but lets NaN through, like the reference's sums)
+__device__ __forceinline__ double clamp0(double v) { return v < 0.0 ? 0.0 : v; }
 __device__ __forceinline__ void chan_norm2(const double* ac, int P, const Unit& un, double* n2) {
-    n2[0] = fmax((ac[0] + ac[1]) / (2.0 * P), 0.0);
-    n2[1] = un.single ? 0.0 : fmax((ac[0] - ac[1]) / (2.0 * P), 0.0);
+    n2[0] = clamp0((ac[0] + ac[1]) / (2.0 * P));
+    n2[1] = un.single ? 0.0 : clamp0((ac[0] - ac[1]) / (2.0 * P));
 }
 
 __global__ void k_init_units(Unit* us, int nb, int B, int single_last, Global* gl) {

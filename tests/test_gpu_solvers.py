@@ -189,3 +189,52 @@ def test_solvers_vs_oracle_config1_scale(sb):
         assert rel(r, ro) <= tol, (algo, rel(r, ro), tol)
         last = slice(-1, None) if algo == "cgls" else slice(None)
         np.testing.assert_allclose(rep.residual_history[last], hist[last], rtol=htol)
+
+
+# ---------------------------------------------------------------- pipeline on the device
+
+
+@pytest.mark.parametrize("algo,iters", [("fbp", 1), ("sirt", 4)])
+def test_pipeline_odd_stack_matches_reference(sb, algo, iters):
+    """run_pipeline on the odd 5-slice stack of test_pipeline.py:131-136
+    against the reference's own pipeline output (golden)."""
+    d = load_golden("pipeline_g32.npz")
+    geom = sb.ScanGeometry(n_p=32, n_theta=12, n_z=5)
+    stack = sb.SinogramStack(data=d["stack"], geometry=geom)
+    cfg = sb.SolverConfig(algorithm=algo, max_iter=iters)
+    vol, rep = sb.run_pipeline(stack, cfg)
+    assert vol.data.shape == (5, 32, 32)
+    assert rel(vol.data, d[f"{algo}_vol"]) <= 1e-3
+    np.testing.assert_allclose(rep.residual_history, d[f"{algo}_res"], rtol=1e-3)
+    assert rep.iterations_run == int(d[f"{algo}_iters"])
+    assert rep.converged == (algo == "fbp")   # tol = 0: SIRT units never report converged
+
+
+def test_pipeline_nan_fault_injection(sb):
+    """test_pipeline.py:151-161: a NaN in slice 0 fails the TV run with the
+    first task's slice range and a NonFinite cause."""
+    from oracle import shepp_logan
+    geom = sb.ScanGeometry(n_p=32, n_theta=12, n_z=8)
+    ops = sb.build_operators(geom, filter_kind="none")
+    data = np.stack([ops.radon(shepp_logan(32)[0] * (1 - 0.05 * k)) for k in range(8)])
+    data[0, 0, 0] = np.nan
+    stack = sb.SinogramStack(data=data, geometry=geom)
+    with pytest.raises(sb.WorkerFailureError) as err:
+        sb.run_pipeline(stack, sb.SolverConfig(algorithm="tv", max_iter=2, filter="none"),
+                        workers=2, ops=ops)
+    assert err.value.slice_range == (0, 4)
+    assert "NonFinite" in str(err.value.cause)
+
+
+def test_pipeline_device_tensor_stack_bitwise_vs_units(sb):
+    """Each pair unit of a pipeline run equals the same pair solved alone."""
+    from oracle import shepp_logan
+    geom = sb.ScanGeometry(n_p=32, n_theta=12, n_z=6)
+    ops = sb.build_operators(geom, filter_kind="hamming")
+    data = np.stack([ops.radon(shepp_logan(32)[0] * (1 - 0.05 * k)) for k in range(6)])
+    cfg = sb.SolverConfig(algorithm="sirt", max_iter=3)
+    vol, _ = sb.run_pipeline(sb.SinogramStack(data=data, geometry=geom), cfg, ops=ops)
+    for u in range(3):
+        rec, _ = sb.solve(data[2 * u] + 1j * data[2 * u + 1], ops, cfg)
+        np.testing.assert_allclose(vol.data[2 * u], rec.real, rtol=0, atol=1e-6)
+        np.testing.assert_allclose(vol.data[2 * u + 1], rec.imag, rtol=0, atol=1e-6)
