@@ -336,7 +336,7 @@ def _sirt_rate(sb, geom, sino_clean, a, dev, stream):
         sino_clean.shape, device=dev, generator=g)
     times = {}
     k1, k2 = 1, max(2, a.sirt_iters)
-    for k in (k1, k2, k1, k2):
+    for k in (k1, k2) * 3:
         cfg = sb.SolverConfig(algorithm="sirt", max_iter=k)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -344,7 +344,7 @@ def _sirt_rate(sb, geom, sino_clean, a, dev, stream):
         _, reps, stat = sb.solvers.solve_batch(noisy, ops_h, cfg, raise_on_failure=False)
         e1.record(stream)
         torch.cuda.synchronize()
-        times[k] = e0.elapsed_time(e1)
+        times[k] = min(times.get(k, float("inf")), e0.elapsed_time(e1))
         its = min(r.iterations_run for r in reps)
     per_iter_ms = (times[k2] - times[k1]) / (k2 - k1)
     return {"value": a.slices * 1e3 / per_iter_ms, "unit": "slice-iterations/s",

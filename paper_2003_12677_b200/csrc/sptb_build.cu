@@ -289,6 +289,151 @@ int build_typed(sptb_plan* p, const BuildArgs& a) {
     return SPTB_OK;
 }
 
+// ---------------------------------------------------------------- patch grouping of S^H
+
+__global__ void k_centers(BuildArgs a, int* cx, int* cy) {
+    const long long N = (long long)a.T * a.P;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < N;
+         s += (long long)gridDim.x * blockDim.x) {
+        double rx, ry, fx, fy;
+        sample_base(a, (int)(s / a.P), (int)(s % a.P), rx, ry, fx, fy);
+        cx[s] = (int)rx;
+        cy[s] = (int)ry;
+    }
+}
+
+// complex64 records {byte offset of the cell in a box plane, re, im, 0} (16 B);
+// complex128 records {cell, 0, re, im} (32 B)  -- see sptb_patch.cu PRec
+__global__ void k_patch_meta_f32(const int* emap, const unsigned* cell, const float2* val,
+                                 void* meta, long long n) {
+    float4* out = reinterpret_cast<float4*>(meta);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float2 v = val[emap[i]];
+        out[i] = make_float4(__uint_as_float(cell[i] * 8u), v.x, v.y, 0.f);
+    }
+}
+__global__ void k_patch_meta_f64(const int* emap, const unsigned* cell, const double2* val,
+                                 void* meta, long long n) {
+    struct alignas(16) Rec { unsigned cell, pad; double2 v; };
+    Rec* out = reinterpret_cast<Rec*>(meta);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Rec r;
+        r.cell = cell[i];
+        r.pad = 0;
+        r.v = val[emap[i]];
+        out[i] = r;
+    }
+}
+
+__global__ void k_map_cols(const int* col, const int* perm, int* out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = perm[col[i]];
+}
+
+// Group S^H rows by the PATCH_W x PATCH_W grid patch of their stencil centre
+// (the rint node of the polar sample, gridding.py:104-121) and record every
+// nonzero by its cell in the patch box.  Host-side bookkeeping, once per plan.
+int build_patches(sptb_plan* p, const BuildArgs& a) {
+    PatchSH& sp = p->shp;
+    const int X = p->X, Y = p->Y;
+    const int64_t N = p->N, nnz = p->SH.nnz;
+    sp.halo = a.W / 2;
+    sp.bw = PATCH_W + 2 * sp.halo;
+    sp.npx = (X + PATCH_W - 1) / PATCH_W;
+    sp.npy = (Y + PATCH_W - 1) / PATCH_W;
+    int *dcx = nullptr, *dcy = nullptr;
+    SPTB_CUDA(cudaMalloc(&dcx, sizeof(int) * N));
+    SPTB_CUDA(cudaMalloc(&dcy, sizeof(int) * N));
+    k_centers<<<grid_of(N), 256, 0, p->stream>>>(a, dcx, dcy);
+    SPTB_LAUNCHED();
+    std::vector<int> cx(N), cy(N), rp(N + 1), col(nnz > 0 ? nnz : 1);
+    SPTB_CUDA(cudaMemcpy(cx.data(), dcx, sizeof(int) * N, cudaMemcpyDeviceToHost));
+    SPTB_CUDA(cudaMemcpy(cy.data(), dcy, sizeof(int) * N, cudaMemcpyDeviceToHost));
+    SPTB_CUDA(cudaMemcpy(rp.data(), p->SH.row_ptr, sizeof(int) * (N + 1), cudaMemcpyDeviceToHost));
+    if (nnz) SPTB_CUDA(cudaMemcpy(col.data(), p->SH.col, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
+    cudaFree(dcx);
+    cudaFree(dcy);
+    const int64_t npatch = (int64_t)sp.npx * sp.npy;
+    std::vector<int> pid(N);
+    std::vector<int64_t> cnt(npatch + 1, 0);
+    for (int64_t s = 0; s < N; ++s) {
+        const int gx = std::min(std::max(cx[s], 0), X - 1), gy = std::min(std::max(cy[s], 0), Y - 1);
+        pid[s] = (gy / PATCH_W) * sp.npx + gx / PATCH_W;
+        cnt[pid[s] + 1]++;
+    }
+    for (int64_t q = 0; q < npatch; ++q) cnt[q + 1] += cnt[q];
+    std::vector<int> order(N), perm(N);
+    {
+        std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t s = 0; s < N; ++s) {  // stable counting sort by patch
+            const int64_t d = fill[pid[s]]++;
+            order[d] = (int)s;
+            perm[s] = (int)d;
+        }
+    }
+    std::vector<int> rpn(N + 1, 0), emap(nnz > 0 ? nnz : 1);
+    std::vector<unsigned> cell(nnz > 0 ? nnz : 1);
+    std::vector<int4> items;
+    int64_t e = 0;
+    for (int64_t q = 0; q < npatch; ++q) {
+        const int bx0 = (int)(q % sp.npx) * PATCH_W - sp.halo, by0 = (int)(q / sp.npx) * PATCH_W - sp.halo;
+        for (int64_t r0 = cnt[q]; r0 < cnt[q + 1]; r0 += PATCH_ITEM_ROWS) {
+            const int64_t r1 = std::min<int64_t>(cnt[q + 1], r0 + PATCH_ITEM_ROWS);
+            const int64_t ebeg = e;
+            for (int64_t r = r0; r < r1; ++r) {
+                const int s = order[r];
+                for (int k = rp[s]; k < rp[s + 1]; ++k) {
+                    const int gx = col[k] % X, gy = col[k] / X;
+                    const int lx = gx - bx0, ly = gy - by0;
+                    if (lx < 0 || lx >= sp.bw || ly < 0 || ly >= sp.bw)
+                        return fail(SPTB_ERR_STATE, "patch build: stencil outside its box");
+                    cell[e] = (unsigned)(ly * sp.bw + lx);
+                    emap[e] = k;
+                    ++e;
+                }
+                rpn[r + 1] = (int)e;
+            }
+            sp.max_item_nnz = std::max<int>(sp.max_item_nnz, (int)(e - ebeg));
+            items.push_back(make_int4((int)q, (int)r0, (int)r1, (int)ebeg));
+        }
+    }
+    sp.n_items = (int64_t)items.size();
+    const size_t rec = p->csize == 16 ? 32 : 16;
+    int* demap = nullptr;
+    unsigned* dcell = nullptr;
+    SPTB_CUDA(cudaMalloc(&sp.items, sizeof(int4) * std::max<size_t>(items.size(), 1)));
+    SPTB_CUDA(cudaMalloc(&sp.rp, sizeof(int) * (N + 1)));
+    SPTB_CUDA(cudaMalloc(&sp.meta, rec * std::max<int64_t>(nnz, 1)));
+    SPTB_CUDA(cudaMalloc(&sp.perm, sizeof(int) * N));
+    SPTB_CUDA(cudaMalloc(&sp.order, sizeof(int) * N));
+    SPTB_CUDA(cudaMalloc(&sp.s_colp, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    SPTB_CUDA(cudaMalloc(&demap, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    SPTB_CUDA(cudaMalloc(&dcell, sizeof(unsigned) * std::max<int64_t>(nnz, 1)));
+    if (!items.empty())
+        SPTB_CUDA(cudaMemcpy(sp.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMemcpy(sp.rp, rpn.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMemcpy(sp.perm, perm.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMemcpy(sp.order, order.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    if (nnz) {
+        SPTB_CUDA(cudaMemcpy(demap, emap.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+        SPTB_CUDA(cudaMemcpy(dcell, cell.data(), sizeof(unsigned) * nnz, cudaMemcpyHostToDevice));
+        if (p->prec == SPTB_PREC_F64)
+            k_patch_meta_f64<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const double2*)p->SH.val, sp.meta, nnz);
+        else
+            k_patch_meta_f32<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const float2*)p->SH.val, sp.meta, nnz);
+        SPTB_LAUNCHED();
+        k_map_cols<<<grid_of(nnz), 256, 0, p->stream>>>(p->S.col, sp.perm, sp.s_colp, nnz);
+        SPTB_LAUNCHED();
+    }
+    SPTB_CUDA(cudaStreamSynchronize(p->stream));
+    cudaFree(demap);
+    cudaFree(dcell);
+    return SPTB_OK;
+}
+
 // ---------------------------------------------------------------- host math
 
 double bessel_i0(double x) {
@@ -437,6 +582,7 @@ int build_matrices(sptb_plan* p, const sptb_geometry* g, const sptb_kernel* k) {
     a.st = dst;
     a.ramp = dramp;
     int rc = (p->prec == SPTB_PREC_F64) ? build_typed<double2>(p, a) : build_typed<float2>(p, a);
+    if (rc == SPTB_OK) rc = build_patches(p, a);
     cudaFree(dct);
     cudaFree(dst);
     cudaFree(dramp);

@@ -83,6 +83,26 @@ struct DevCSR {
     int64_t n_unique = 0;
 };
 
+// S^H regrouped by grid patch: every sample is assigned to the PATCH_W x
+// PATCH_W grid patch holding its stencil centre, so all of its nonzeros fall in
+// the patch's box (patch + halo of width/2 cells).  Samples are renumbered
+// s' (patch-major, stable); work items cover <= PATCH_ITEM_ROWS samples of one
+// patch.  Nonzeros are stored as (box-local cell, value) records.
+constexpr int PATCH_W = 8;
+constexpr int PATCH_ITEM_ROWS = 96;
+
+struct PatchSH {
+    int halo = 1, bw = 10, npx = 0, npy = 0;
+    int64_t n_items = 0;
+    int max_item_nnz = 0;
+    int4* items = nullptr;    // {patch id, row begin (s'), row end, entry begin}
+    int* rp = nullptr;        // N + 1, row pointers in s' order
+    void* meta = nullptr;     // nnz records {u32 cell, u32 pad, complex val}
+    int* perm = nullptr;      // perm[s] = s'
+    int* order = nullptr;     // order[s'] = s
+    int* s_colp = nullptr;    // S column indices renumbered to s'
+};
+
 struct FFTPlans {
     cufftHandle fft2 = 0;   // Y x X, batch B, [b][y][x]
     cufftHandle fft1 = 0;   // n_p,   batch B*T, [b][t][p]
@@ -102,6 +122,7 @@ struct sptb_plan {
     size_t csize = 8;          // bytes per complex element
 
     sptb::DevCSR S, SH;        // S: M x N rows=grid, SH: N x M rows=samples
+    sptb::PatchSH shp;         // patch-grouped S^H (the production forward SpMM)
     void* SW_val = nullptr;    // S values with the filter folded (nullptr: none)
     std::vector<double> w_host;  // filter weights (n_p or N), empty = none
     void* w_dev = nullptr;       // real weights of plan precision (n_p or N)
@@ -156,6 +177,24 @@ int launch_spmm(const DevCSR& A, const void* val, const void* x, void* y, int B,
 
 template <typename R>
 int launch_transpose_bm_to_mb(const void* in, void* out, int B, int64_t M, cudaStream_t st);
+
+// patch-grouped S^H: x [b][m] (batch-outer) -> y [s'][b]; sub: y = sub - S^H x
+template <typename R>
+int launch_spmm_sh_patch(const sptb_plan* p, const void* x_bm, void* y_sb, int B, const void* sub,
+                         cudaStream_t st);
+// [b][s] -> [perm[s]][b]   and   [s'][b] -> [b][order[s']]
+template <typename R>
+int launch_transpose_permute(const void* in_bs, void* out_sb, const int* perm, int B, int64_t N,
+                             cudaStream_t st);
+template <typename R>
+int launch_transpose_unpermute(const void* in_sb, void* out_bs, const int* order, int B, int64_t N,
+                               cudaStream_t st);
+// S with columns renumbered to the patch order s'
+inline DevCSR s_permuted(const sptb_plan* p) {
+    DevCSR A = p->S;
+    A.col = p->shp.s_colp;
+    return A;
+}
 
 // pack caller slices -> complex [b][len] (optionally times a real plane)
 // unpack complex [b][len] -> caller slices, times plane (optional) * scale

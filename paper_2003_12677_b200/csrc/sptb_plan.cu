@@ -184,12 +184,9 @@ int radon_batch(sptb_plan* p, const void* in, int in_fmt, int64_t n, int64_t u0,
     cudaStream_t st = p->stream;
     SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->M, p->deapo, p->G0, st));
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_FORWARD));
-    const void* x = p->G0;
-    if (B > 1) {
-        SPTB_TRY(launch_transpose_bm_to_mb<R>(p->G0, p->G1, B, p->M, st));
-        x = p->G1;
-    }
-    SPTB_TRY(launch_spmm<R>(p->SH, p->SH.val, x, p->S0, B, true, nullptr, st));
+    // patch SpMM reads the batch-outer FFT2 output directly -> [s'][b]
+    SPTB_TRY(launch_spmm_sh_patch<R>(p, p->G0, p->S1, B, nullptr, st));
+    SPTB_TRY(launch_transpose_unpermute<R>(p->S1, p->S0, p->shp.order, B, p->N, st));
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_INVERSE));
     return launch_unpack<R>(p->S0, p->N, nullptr, 1.0 / p->P, out, out_fmt, on, ou0, nb, st);
 }
@@ -203,13 +200,9 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     cudaStream_t st = p->stream;
     SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
-    const void* x = p->S0;
-    if (B > 1) {
-        SPTB_TRY(launch_transpose_bm_to_mb<R>(p->S0, p->S1, B, p->N, st));
-        x = p->S1;
-    }
+    SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
     const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-    SPTB_TRY(launch_spmm<R>(p->S, vals, x, p->G0, B, true, nullptr, st));
+    SPTB_TRY(launch_spmm<R>(s_permuted(p), vals, p->S1, p->G0, B, true, nullptr, st));
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_INVERSE));
     return launch_unpack<R>(p->G0, p->M, p->deapo, scale / p->P, out, out_fmt, on, ou0, nb, st);
 }
@@ -311,7 +304,9 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->SW_val, p->w_dev, p->deapo, p->G0, p->G1, p->G2, p->S0, p->S1,
                     p->stage_in, p->stage_out, p->red, p->fft_work,
                     p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
-                    p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc};
+                    p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc,
+                    p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
+                    p->shp.s_colp};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->extra)

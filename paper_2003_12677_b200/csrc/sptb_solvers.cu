@@ -557,7 +557,8 @@ struct OpTvShrink {
 template <typename R, typename RV, bool UPDATE>
 __global__ void __launch_bounds__(RT)
 k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
-       typename CT<R>::T* __restrict__ rf, const R* __restrict__ w, long long wlen, int T, int P,
+       typename CT<R>::T* __restrict__ rf, const int* __restrict__ perm,
+       const R* __restrict__ w, long long wlen, int T, int P,
        int B, const Unit* __restrict__ us, double* __restrict__ part) {
     const int H = P / 2 + 1;
     const long long total = (long long)T * H * B;
@@ -580,8 +581,8 @@ k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
         const int jh = e / B;
         const int j1 = jh, j2 = (P - jh) % P;
         if (j1 > j2 && j2 != 0) continue;  // odd P: each pair once
-        const size_t s1 = (size_t)t * P + j1, s2 = (size_t)t * P + j2;
-        const double wt = w ? (double)(wlen == P ? w[j1] : w[s1]) : 1.0;
+        const size_t s1 = (size_t)perm[(size_t)t * P + j1], s2 = (size_t)perm[(size_t)t * P + j2];
+        const double wt = w ? (double)(wlen == P ? w[j1] : w[(size_t)t * P + j1]) : 1.0;
         D2 r1 = d2(rh[s1 * B + b]);
         D2 r2 = d2(rh[s2 * B + b]);
         if (UPDATE && step) {
@@ -1011,7 +1012,7 @@ struct Solver {
 
     template <bool UPDATE, typename RV>
     int spec(RV* rh, const C* qh, C* rf, double* out_sums) {
-        k_spec<R, RV, UPDATE><<<nblk_spec, RT, 0, st>>>(rh, qh, rf, (const R*)p->w_dev, p->w_len,
+        k_spec<R, RV, UPDATE><<<nblk_spec, RT, 0, st>>>(rh, qh, rf, p->shp.perm, (const R*)p->w_dev, p->w_len,
                                                         p->T, p->P, B, us, part);
         SPTB_LAUNCHED();
         k_finish<<<(B * 2 * 32 + 255) / 256, 256, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
@@ -1033,12 +1034,8 @@ struct Solver {
         FFTPlans* f;
         SPTB_TRY(get_fft(p, B, &f));
         SPTB_TRY(fft(f->fft2, W, CUFFT_FORWARD));
-        const void* x = W;
-        if (B > 1) {
-            SPTB_TRY(launch_transpose_bm_to_mb<R>(W, p->G1, B, p->M, st));
-            x = p->G1;
-        }
-        return launch_spmm<R>(p->SH, p->SH.val, x, out, B, false, sub, st);
+        // patch-grouped S^H reads the batch-outer FFT2 output directly
+        return launch_spmm_sh_patch<R>(p, W, out, B, sub, st);
     }
 
     // W[b][m] = IFFT2(S_(w) rh)   (caller applies deapo/P)
@@ -1046,7 +1043,7 @@ struct Solver {
         FFTPlans* f;
         SPTB_TRY(get_fft(p, B, &f));
         const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-        SPTB_TRY(launch_spmm<R>(p->S, vals, rh, W, B, true, nullptr, st));
+        SPTB_TRY(launch_spmm<R>(s_permuted(p), vals, rh, W, B, true, nullptr, st));
         return fft(f->fft2, W, CUFFT_INVERSE);
     }
 
@@ -1056,9 +1053,7 @@ struct Solver {
         SPTB_TRY(get_fft(p, B, &f));
         SPTB_TRY(launch_pack<R>(in, fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
         SPTB_TRY(fft(f->fft1, p->S0, CUFFT_FORWARD));
-        if (B > 1) return launch_transpose_bm_to_mb<R>(p->S0, BH, B, p->N, st);
-        SPTB_CUDA(cudaMemcpyAsync(BH, p->S0, sizeof(C) * p->N, cudaMemcpyDeviceToDevice, st));
-        return SPTB_OK;
+        return launch_transpose_permute<R>(p->S0, BH, p->shp.perm, B, p->N, st);
     }
 
     int unit_kernel_done() {
