@@ -62,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     if _newer(objs, LIB) or force:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", CUDA_LIB, "-lcufft",
-               "-Xlinker", "-rpath," + CUDA_LIB]
+               "-Xlinker", "-rpath," + CUDA_LIB, "-Xlinker", "--no-undefined"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

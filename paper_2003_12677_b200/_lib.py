@@ -12,7 +12,8 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsptb.so")
+# SPTB_LIB_VARIANT: an alternative in-tree build (kernel tuning experiments)
+LIB_PATH = os.path.join(_HERE, os.environ.get("SPTB_LIB_VARIANT", "libsptb.so"))
 
 OK, ERR_SHAPE, ERR_ARG, ERR_NEAR_ZERO, ERR_CUDA, ERR_CUFFT, ERR_OOM, ERR_NONFINITE, \
     ERR_DIVERGENCE, ERR_STATE = range(10)

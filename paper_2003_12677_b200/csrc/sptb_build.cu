@@ -333,8 +333,31 @@ __global__ void k_map_cols(const int* col, const int* perm, int* out, long long 
         out[i] = perm[col[i]];
 }
 
+// slot-mode rows: sval[r][k] = S^H value of entry src[r*10+k] (zero when < 0);
+// slot 9 carries the box cell of the block origin in .x
+template <typename C>
+__global__ void k_slot_vals(const int* src, const int* base, const C* val, C* out, long long nrows) {
+    const long long n = nrows * SLOT_STRIDE;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / SLOT_STRIDE;
+        const int k = (int)(i - r * SLOT_STRIDE);
+        C v;
+        v.x = 0;
+        v.y = 0;
+        if (k == 9) {
+            if (sizeof(v.x) == 4) v.x = __int_as_float(base[r]);
+            else v.x = __longlong_as_double((long long)base[r]);
+        } else if (src[i] >= 0) {
+            v = val[src[i]];
+        }
+        out[i] = v;
+    }
+}
+
 // Group S^H rows by the PATCH_W x PATCH_W grid patch of their stencil centre
-// (the rint node of the polar sample, gridding.py:104-121) and record every
+// (the rint node of the polar sample, gridding.py:104-121).  Slot mode (kernel
+// width 3) stores each regular row as 9 fixed slots; record mode stores every
 // nonzero by its cell in the patch box.  Host-side bookkeeping, once per plan.
 int build_patches(sptb_plan* p, const BuildArgs& a) {
     PatchSH& sp = p->shp;
@@ -344,6 +367,7 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     sp.bw = PATCH_W + 2 * sp.halo;
     sp.npx = (X + PATCH_W - 1) / PATCH_W;
     sp.npy = (Y + PATCH_W - 1) / PATCH_W;
+    sp.slot_mode = (a.W == 3) ? 1 : 0;
     int *dcx = nullptr, *dcy = nullptr;
     SPTB_CUDA(cudaMalloc(&dcx, sizeof(int) * N));
     SPTB_CUDA(cudaMalloc(&dcy, sizeof(int) * N));
@@ -358,13 +382,31 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     cudaFree(dcy);
     const int64_t npatch = (int64_t)sp.npx * sp.npy;
     std::vector<int> pid(N);
-    std::vector<int64_t> cnt(npatch + 1, 0);
+    std::vector<int> base(sp.slot_mode ? N : 0);
+    std::vector<int64_t> cnt(npatch + 2, 0);  // last bucket: irregular rows
     for (int64_t s = 0; s < N; ++s) {
         const int gx = std::min(std::max(cx[s], 0), X - 1), gy = std::min(std::max(cy[s], 0), Y - 1);
-        pid[s] = (gy / PATCH_W) * sp.npx + gx / PATCH_W;
-        cnt[pid[s] + 1]++;
+        int q = (gy / PATCH_W) * sp.npx + gx / PATCH_W;
+        if (sp.slot_mode) {
+            // slot-mode patches are shifted one cell in x (patch px covers x in
+            // [8px+1, 8px+8], box origin 8px): the TMA box origin must sit on a
+            // 16-byte boundary of the grid row
+            const int px = std::min(std::max(gx - 1, 0) / PATCH_W, sp.npx - 1);
+            q = (gy / PATCH_W) * sp.npx + px;
+            const int bx0 = px * PATCH_W, by0 = (q / sp.npx) * PATCH_W - sp.halo;
+            const int lx0 = cx[s] - 1 - bx0, ly0 = cy[s] - 1 - by0;
+            bool reg = lx0 >= 0 && lx0 + 2 < sp.bw && ly0 >= 0 && ly0 + 2 < sp.bw;
+            for (int k = rp[s]; reg && k < rp[s + 1]; ++k) {
+                const int ex = col[k] % X - cx[s], ey = col[k] / X - cy[s];
+                reg = ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1;
+            }
+            if (!reg) q = (int)npatch;
+            base[s] = reg ? ly0 * sp.bw + lx0 : 0;
+        }
+        pid[s] = q;
+        cnt[q + 1]++;
     }
-    for (int64_t q = 0; q < npatch; ++q) cnt[q + 1] += cnt[q];
+    for (int64_t q = 0; q <= npatch; ++q) cnt[q + 1] += cnt[q];
     std::vector<int> order(N), perm(N);
     {
         std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
@@ -374,63 +416,126 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
             perm[s] = (int)d;
         }
     }
-    std::vector<int> rpn(N + 1, 0), emap(nnz > 0 ? nnz : 1);
-    std::vector<unsigned> cell(nnz > 0 ? nnz : 1);
-    std::vector<int4> items;
-    int64_t e = 0;
-    for (int64_t q = 0; q < npatch; ++q) {
-        const int bx0 = (int)(q % sp.npx) * PATCH_W - sp.halo, by0 = (int)(q / sp.npx) * PATCH_W - sp.halo;
-        for (int64_t r0 = cnt[q]; r0 < cnt[q + 1]; r0 += PATCH_ITEM_ROWS) {
-            const int64_t r1 = std::min<int64_t>(cnt[q + 1], r0 + PATCH_ITEM_ROWS);
-            const int64_t ebeg = e;
-            for (int64_t r = r0; r < r1; ++r) {
-                const int s = order[r];
-                for (int k = rp[s]; k < rp[s + 1]; ++k) {
-                    const int gx = col[k] % X, gy = col[k] / X;
-                    const int lx = gx - bx0, ly = gy - by0;
-                    if (lx < 0 || lx >= sp.bw || ly < 0 || ly >= sp.bw)
-                        return fail(SPTB_ERR_STATE, "patch build: stencil outside its box");
-                    cell[e] = (unsigned)(ly * sp.bw + lx);
-                    emap[e] = k;
-                    ++e;
-                }
-                rpn[r + 1] = (int)e;
+    sp.n_reg = sp.slot_mode ? cnt[npatch] : N;
+    if (sp.slot_mode) {
+        // within a patch, alternate rows whose block origin has even and odd x:
+        // two rows sharing a half-warp then read cells of opposite parity, which
+        // keeps the box reads of the TMA kernel (even plane stride) conflict free
+        std::vector<int> ev, od;
+        for (int64_t q = 0; q < npatch; ++q) {
+            ev.clear();
+            od.clear();
+            for (int64_t r = cnt[q]; r < cnt[q + 1]; ++r) (cx[order[r]] & 1 ? od : ev).push_back(order[r]);
+            size_t ie = 0, io = 0;
+            for (int64_t r = cnt[q]; r < cnt[q + 1]; ++r) {
+                const bool take_even = (ie < ev.size()) && ((r - cnt[q]) % 2 == 0 || io >= od.size());
+                const int s = take_even ? ev[ie++] : od[io++];
+                order[r] = s;
+                perm[s] = (int)r;
             }
-            sp.max_item_nnz = std::max<int>(sp.max_item_nnz, (int)(e - ebeg));
-            items.push_back(make_int4((int)q, (int)r0, (int)r1, (int)ebeg));
+        }
+    }
+    std::vector<int4> items;
+    std::vector<int> rpn, emap, slot_src;
+    std::vector<unsigned> cell;
+    if (sp.slot_mode) {
+        slot_src.assign((size_t)std::max<int64_t>(sp.n_reg, 1) * SLOT_STRIDE, -1);
+        std::vector<int> base_r(std::max<int64_t>(sp.n_reg, 1), 0);
+        for (int64_t r = 0; r < sp.n_reg; ++r) {
+            const int s = order[r];
+            base_r[r] = base[s];
+            for (int k = rp[s]; k < rp[s + 1]; ++k) {
+                const int ex = col[k] % X - cx[s], ey = col[k] / X - cy[s];
+                slot_src[(size_t)r * SLOT_STRIDE + (ey + 1) * 3 + (ex + 1)] = k;
+            }
+        }
+        for (int64_t q = 0; q < npatch; ++q)
+            for (int64_t r0 = cnt[q]; r0 < cnt[q + 1]; r0 += PATCH_ITEM_ROWS)
+                items.push_back(make_int4((int)q, (int)r0, (int)std::min<int64_t>(cnt[q + 1], r0 + PATCH_ITEM_ROWS), 0));
+        // full items (the dense centre) launch first so the long CTAs do not
+        // form the tail; spatial order is kept within both groups (L2 reuse of halos)
+        std::stable_partition(items.begin(), items.end(),
+                              [](const int4& it) { return it.z - it.y == PATCH_ITEM_ROWS; });
+        int *dsrc = nullptr, *dbase = nullptr;
+        SPTB_CUDA(cudaMalloc(&dsrc, sizeof(int) * slot_src.size()));
+        SPTB_CUDA(cudaMalloc(&dbase, sizeof(int) * base_r.size()));
+        SPTB_CUDA(cudaMalloc(&sp.sval, p->csize * slot_src.size()));
+        SPTB_CUDA(cudaMemcpy(dsrc, slot_src.data(), sizeof(int) * slot_src.size(), cudaMemcpyHostToDevice));
+        SPTB_CUDA(cudaMemcpy(dbase, base_r.data(), sizeof(int) * base_r.size(), cudaMemcpyHostToDevice));
+        if (p->prec == SPTB_PREC_F64)
+            k_slot_vals<double2><<<grid_of((long long)slot_src.size()), 256, 0, p->stream>>>(
+                dsrc, dbase, (const double2*)p->SH.val, (double2*)sp.sval, sp.n_reg);
+        else
+            k_slot_vals<float2><<<grid_of((long long)slot_src.size()), 256, 0, p->stream>>>(
+                dsrc, dbase, (const float2*)p->SH.val, (float2*)sp.sval, sp.n_reg);
+        SPTB_LAUNCHED();
+        SPTB_CUDA(cudaStreamSynchronize(p->stream));
+        cudaFree(dsrc);
+        cudaFree(dbase);
+    } else {
+        rpn.assign(N + 1, 0);
+        emap.assign(nnz > 0 ? nnz : 1, 0);
+        cell.assign(nnz > 0 ? nnz : 1, 0);
+        int64_t e = 0;
+        for (int64_t q = 0; q < npatch; ++q) {
+            const int bx0 = (int)(q % sp.npx) * PATCH_W - sp.halo, by0 = (int)(q / sp.npx) * PATCH_W - sp.halo;
+            for (int64_t r0 = cnt[q]; r0 < cnt[q + 1]; r0 += PATCH_ITEM_ROWS) {
+                const int64_t r1 = std::min<int64_t>(cnt[q + 1], r0 + PATCH_ITEM_ROWS);
+                const int64_t ebeg = e;
+                for (int64_t r = r0; r < r1; ++r) {
+                    const int s = order[r];
+                    for (int k = rp[s]; k < rp[s + 1]; ++k) {
+                        const int gx = col[k] % X, gy = col[k] / X;
+                        const int lx = gx - bx0, ly = gy - by0;
+                        if (lx < 0 || lx >= sp.bw || ly < 0 || ly >= sp.bw)
+                            return fail(SPTB_ERR_STATE, "patch build: stencil outside its box");
+                        cell[e] = (unsigned)(ly * sp.bw + lx);
+                        emap[e] = k;
+                        ++e;
+                    }
+                    rpn[r + 1] = (int)e;
+                }
+                sp.max_item_nnz = std::max<int>(sp.max_item_nnz, (int)(e - ebeg));
+                items.push_back(make_int4((int)q, (int)r0, (int)r1, (int)ebeg));
+            }
         }
     }
     sp.n_items = (int64_t)items.size();
-    const size_t rec = p->csize == 16 ? 32 : 16;
-    int* demap = nullptr;
-    unsigned* dcell = nullptr;
     SPTB_CUDA(cudaMalloc(&sp.items, sizeof(int4) * std::max<size_t>(items.size(), 1)));
-    SPTB_CUDA(cudaMalloc(&sp.rp, sizeof(int) * (N + 1)));
-    SPTB_CUDA(cudaMalloc(&sp.meta, rec * std::max<int64_t>(nnz, 1)));
     SPTB_CUDA(cudaMalloc(&sp.perm, sizeof(int) * N));
     SPTB_CUDA(cudaMalloc(&sp.order, sizeof(int) * N));
     SPTB_CUDA(cudaMalloc(&sp.s_colp, sizeof(int) * std::max<int64_t>(nnz, 1)));
-    SPTB_CUDA(cudaMalloc(&demap, sizeof(int) * std::max<int64_t>(nnz, 1)));
-    SPTB_CUDA(cudaMalloc(&dcell, sizeof(unsigned) * std::max<int64_t>(nnz, 1)));
     if (!items.empty())
         SPTB_CUDA(cudaMemcpy(sp.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
-    SPTB_CUDA(cudaMemcpy(sp.rp, rpn.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice));
     SPTB_CUDA(cudaMemcpy(sp.perm, perm.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
     SPTB_CUDA(cudaMemcpy(sp.order, order.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    if (!sp.slot_mode) {
+        const size_t rec = p->csize == 16 ? 32 : 16;
+        int* demap = nullptr;
+        unsigned* dcell = nullptr;
+        SPTB_CUDA(cudaMalloc(&sp.rp, sizeof(int) * (N + 1)));
+        SPTB_CUDA(cudaMalloc(&sp.meta, rec * std::max<int64_t>(nnz, 1)));
+        SPTB_CUDA(cudaMalloc(&demap, sizeof(int) * std::max<int64_t>(nnz, 1)));
+        SPTB_CUDA(cudaMalloc(&dcell, sizeof(unsigned) * std::max<int64_t>(nnz, 1)));
+        SPTB_CUDA(cudaMemcpy(sp.rp, rpn.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice));
+        if (nnz) {
+            SPTB_CUDA(cudaMemcpy(demap, emap.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+            SPTB_CUDA(cudaMemcpy(dcell, cell.data(), sizeof(unsigned) * nnz, cudaMemcpyHostToDevice));
+            if (p->prec == SPTB_PREC_F64)
+                k_patch_meta_f64<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const double2*)p->SH.val, sp.meta, nnz);
+            else
+                k_patch_meta_f32<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const float2*)p->SH.val, sp.meta, nnz);
+            SPTB_LAUNCHED();
+        }
+        SPTB_CUDA(cudaStreamSynchronize(p->stream));
+        cudaFree(demap);
+        cudaFree(dcell);
+    }
     if (nnz) {
-        SPTB_CUDA(cudaMemcpy(demap, emap.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-        SPTB_CUDA(cudaMemcpy(dcell, cell.data(), sizeof(unsigned) * nnz, cudaMemcpyHostToDevice));
-        if (p->prec == SPTB_PREC_F64)
-            k_patch_meta_f64<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const double2*)p->SH.val, sp.meta, nnz);
-        else
-            k_patch_meta_f32<<<grid_of(nnz), 256, 0, p->stream>>>(demap, dcell, (const float2*)p->SH.val, sp.meta, nnz);
-        SPTB_LAUNCHED();
         k_map_cols<<<grid_of(nnz), 256, 0, p->stream>>>(p->S.col, sp.perm, sp.s_colp, nnz);
         SPTB_LAUNCHED();
     }
     SPTB_CUDA(cudaStreamSynchronize(p->stream));
-    cudaFree(demap);
-    cudaFree(dcell);
     return SPTB_OK;
 }
 

@@ -89,15 +89,29 @@ struct DevCSR {
 // s' (patch-major, stable); work items cover <= PATCH_ITEM_ROWS samples of one
 // patch.  Nonzeros are stored as (box-local cell, value) records.
 constexpr int PATCH_W = 8;
-constexpr int PATCH_ITEM_ROWS = 96;
+#ifndef SPTB_ITEM_ROWS
+#define SPTB_ITEM_ROWS 64
+#endif
+constexpr int PATCH_ITEM_ROWS = SPTB_ITEM_ROWS;
+
+// Slot mode (kernel width 3): a sample's nonzeros all lie in the 3x3 block
+// around its stencil centre, so a row is stored as 9 fixed slots (pruned
+// entries are zero) plus the box cell of the block origin in a tenth slot:
+// no per-nonzero index, and the cell offsets of the slots are compile-time
+// constants.  Rows whose block leaves their patch box ("irregular": centre
+// outside the grid) are numbered last and handled by a direct-gather kernel.
+constexpr int SLOT_STRIDE = 10;  // complex elements per slot-mode row
 
 struct PatchSH {
     int halo = 1, bw = 10, npx = 0, npy = 0;
+    int slot_mode = 0;        // 1: sval/irregular layout, 0: records (meta/rp)
     int64_t n_items = 0;
+    int64_t n_reg = 0;        // slot mode: rows [0, n_reg) are in items, the rest irregular
     int max_item_nnz = 0;
     int4* items = nullptr;    // {patch id, row begin (s'), row end, entry begin}
-    int* rp = nullptr;        // N + 1, row pointers in s' order
-    void* meta = nullptr;     // nnz records {u32 cell, u32 pad, complex val}
+    int* rp = nullptr;        // N + 1, row pointers in s' order (record mode)
+    void* meta = nullptr;     // nnz records {u32 cell, u32 pad, complex val} (record mode)
+    void* sval = nullptr;     // slot mode: [n_reg][SLOT_STRIDE] complex, slot 9 .x = base cell bits
     int* perm = nullptr;      // perm[s] = s'
     int* order = nullptr;     // order[s'] = s
     int* s_colp = nullptr;    // S column indices renumbered to s'

@@ -306,7 +306,7 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
                     p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
-                    p->shp.s_colp};
+                    p->shp.s_colp, p->shp.sval};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->extra)
