@@ -395,10 +395,11 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
             q = (gy / PATCH_W) * sp.npx + px;
             const int bx0 = px * PATCH_W, by0 = (q / sp.npx) * PATCH_W - sp.halo;
             const int lx0 = cx[s] - 1 - bx0, ly0 = cy[s] - 1 - by0;
-            bool reg = lx0 >= 0 && lx0 + 2 < sp.bw && ly0 >= 0 && ly0 + 2 < sp.bw;
-            for (int k = rp[s]; reg && k < rp[s + 1]; ++k) {
+            const bool reg = lx0 >= 0 && lx0 + 2 < sp.bw && ly0 >= 0 && ly0 + 2 < sp.bw;
+            for (int k = rp[s]; k < rp[s + 1]; ++k) {
                 const int ex = col[k] % X - cx[s], ey = col[k] / X - cy[s];
-                reg = ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1;
+                if (ex < -1 || ex > 1 || ey < -1 || ey > 1)
+                    return fail(SPTB_ERR_STATE, "slot build: stencil entry outside the 3x3 block");
             }
             if (!reg) q = (int)npatch;
             base[s] = reg ? ly0 * sp.bw + lx0 : 0;
@@ -439,9 +440,11 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     std::vector<int> rpn, emap, slot_src;
     std::vector<unsigned> cell;
     if (sp.slot_mode) {
-        slot_src.assign((size_t)std::max<int64_t>(sp.n_reg, 1) * SLOT_STRIDE, -1);
-        std::vector<int> base_r(std::max<int64_t>(sp.n_reg, 1), 0);
-        for (int64_t r = 0; r < sp.n_reg; ++r) {
+        // slot rows for every sample (irregular rows too: the output-tiled S
+        // reads them; their base is unused)
+        slot_src.assign((size_t)std::max<int64_t>(N, 1) * SLOT_STRIDE, -1);
+        std::vector<int> base_r(std::max<int64_t>(N, 1), 0);
+        for (int64_t r = 0; r < N; ++r) {
             const int s = order[r];
             base_r[r] = base[s];
             for (int k = rp[s]; k < rp[s + 1]; ++k) {
@@ -464,10 +467,10 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         SPTB_CUDA(cudaMemcpy(dbase, base_r.data(), sizeof(int) * base_r.size(), cudaMemcpyHostToDevice));
         if (p->prec == SPTB_PREC_F64)
             k_slot_vals<double2><<<grid_of((long long)slot_src.size()), 256, 0, p->stream>>>(
-                dsrc, dbase, (const double2*)p->SH.val, (double2*)sp.sval, sp.n_reg);
+                dsrc, dbase, (const double2*)p->SH.val, (double2*)sp.sval, N);
         else
             k_slot_vals<float2><<<grid_of((long long)slot_src.size()), 256, 0, p->stream>>>(
-                dsrc, dbase, (const float2*)p->SH.val, (float2*)sp.sval, sp.n_reg);
+                dsrc, dbase, (const float2*)p->SH.val, (float2*)sp.sval, N);
         SPTB_LAUNCHED();
         SPTB_CUDA(cudaStreamSynchronize(p->stream));
         cudaFree(dsrc);
@@ -536,6 +539,7 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         SPTB_LAUNCHED();
     }
     SPTB_CUDA(cudaStreamSynchronize(p->stream));
+    if (sp.slot_mode) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order));
     return SPTB_OK;
 }
 
@@ -739,6 +743,7 @@ int fold_filter(sptb_plan* p) {
         p->SW_val = nullptr;
     }
     SPTB_TRY(upload_weights(p));
+    SPTB_TRY(fold_slot_filter(p));
     if (p->w_len == 0) return SPTB_OK;
     SPTB_CUDA(cudaMalloc(&p->SW_val, cs * (nnz > 0 ? nnz : 1)));
     if (nnz == 0) return SPTB_OK;

@@ -117,6 +117,25 @@ struct PatchSH {
     int* s_colp = nullptr;    // S column indices renumbered to s'
 };
 
+// S (grid <- samples) by 8x8 output tiles: a tile lists the samples whose
+// 3x3 block touches it (ascending s', in chunks of <= STILE_CHUNK), and per
+// chunk a metadata block of u32: 65 cell pointers (relative to the entry
+// start) followed by entries (local << 16 | local * 10 + slot), padded to 16 B.
+// Values come from the slot rows (conj(S^H) = S), unfiltered or w-folded.
+constexpr int STILE = 8;
+constexpr int STILE_CHUNK = 128;
+
+struct STiles {
+    int ntx = 0, nty = 0;
+    int64_t n_chunks = 0;
+    int* tile_chunk = nullptr;   // ntiles + 1 chunk offsets
+    int4* chunks = nullptr;      // {tile, sample begin, n samples, meta offset (u32 units)}
+    int* samp = nullptr;         // s' lists
+    unsigned* meta = nullptr;
+    int max_meta = 0;            // largest metadata block (u32 units)
+    void* swval = nullptr;       // slot rows with the filter folded (w[s] * sval)
+};
+
 struct FFTPlans {
     cufftHandle fft2 = 0;   // Y x X, batch B, [b][y][x]
     cufftHandle fft1 = 0;   // n_p,   batch B*T, [b][t][p]
@@ -137,6 +156,7 @@ struct sptb_plan {
 
     sptb::DevCSR S, SH;        // S: M x N rows=grid, SH: N x M rows=samples
     sptb::PatchSH shp;         // patch-grouped S^H (the production forward SpMM)
+    sptb::STiles stl;          // output-tiled S (the production adjoint SpMM)
     void* SW_val = nullptr;    // S values with the filter folded (nullptr: none)
     std::vector<double> w_host;  // filter weights (n_p or N), empty = none
     void* w_dev = nullptr;       // real weights of plan precision (n_p or N)
@@ -158,6 +178,13 @@ struct sptb_plan {
     size_t stage_in_bytes = 0;
     void* stage_out = nullptr;
     size_t stage_out_bytes = 0;
+    // pipelined host I/O (drive(): H2D / compute / D2H of successive chunks overlap)
+    static constexpr int NPIPE = 3;
+    cudaStream_t io_in = nullptr, io_out = nullptr;
+    cudaEvent_t ev_in[NPIPE] = {}, ev_comp[NPIPE] = {}, ev_out[NPIPE] = {}, ev_start = nullptr;
+    void* pin[NPIPE] = {};
+    void* pout[NPIPE] = {};
+    size_t pin_bytes[NPIPE] = {}, pout_bytes[NPIPE] = {};
     // reduction scratch
     double* red = nullptr;
     size_t red_len = 0;
@@ -203,6 +230,15 @@ int launch_transpose_permute(const void* in_bs, void* out_sb, const int* perm, i
 template <typename R>
 int launch_transpose_unpermute(const void* in_sb, void* out_bs, const int* order, int B, int64_t N,
                                cudaStream_t st);
+// Y[b][m] = S_(w) X, X [s'][b]: output-tiled kernel when the slot layout
+// exists (vals == S.val -> slot rows, vals == SW_val -> w-folded slot rows),
+// else the row-gather kernel over S with columns renumbered to s'
+template <typename R>
+int launch_spmm_s(const sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B,
+                  cudaStream_t st);
+int build_stiles(sptb_plan* p, const std::vector<int>& cx, const std::vector<int>& cy,
+                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order);
+int fold_slot_filter(sptb_plan* p);
 // S with columns renumbered to the patch order s'
 inline DevCSR s_permuted(const sptb_plan* p) {
     DevCSR A = p->S;

@@ -127,6 +127,25 @@ static size_t slice_bytes(int fmt, int64_t len) {
 }
 
 // Generic driver: host pointers are staged per batch through device buffers.
+static int ensure_pipe(sptb_plan* p) {
+    if (p->io_in) return SPTB_OK;
+    SPTB_CUDA(cudaStreamCreateWithFlags(&p->io_in, cudaStreamNonBlocking));
+    SPTB_CUDA(cudaStreamCreateWithFlags(&p->io_out, cudaStreamNonBlocking));
+    for (int k = 0; k < sptb_plan::NPIPE; ++k) {
+        SPTB_CUDA(cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming));
+        SPTB_CUDA(cudaEventCreateWithFlags(&p->ev_comp[k], cudaEventDisableTiming));
+        SPTB_CUDA(cudaEventCreateWithFlags(&p->ev_out[k], cudaEventDisableTiming));
+    }
+    SPTB_CUDA(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+    return SPTB_OK;
+}
+
+// Generic driver over batches of `units` (complex vectors).  Device pointers:
+// one pass per max_batch units on the plan stream.  Host pointers: the units
+// are cut into >= 4 chunks and run as a three-stage pipeline -- H2D of chunk
+// i+1 (io_in stream), compute of chunk i (plan stream), D2H of chunk i-1
+// (io_out stream) -- through NPIPE rotating staging buffers, so the PCIe
+// transfers in both directions overlap each other and the kernels.
 template <typename F>
 static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void* out,
                  int out_fmt, int64_t out_len, int64_t n, F&& body) {
@@ -134,44 +153,64 @@ static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void*
         return fail(SPTB_ERR_ARG, "output kind (real/complex) must match the input's");
     if (n < 0) return fail(SPTB_ERR_ARG, "negative slice count");
     if (n == 0) return SPTB_OK;
-    SPTB_TRY(ensure_work(p, pow2_at_least((int)std::min<int64_t>(p->max_batch, n_units(in_fmt, n)))));
     bool din = true, dout = true;
     is_device_ptr(in, &din);
     is_device_ptr(out, &dout);
     const int64_t units = n_units(in_fmt, n);
-    for (int64_t u0 = 0; u0 < units; u0 += p->max_batch) {
-        const int nb = (int)std::min<int64_t>(p->max_batch, units - u0);
-        const int B = pow2_at_least(nb);
+    int64_t chunk = p->max_batch;
+    if (!din || !dout) chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, (units + 3) / 4));
+    SPTB_TRY(ensure_work(p, pow2_at_least((int)std::min<int64_t>(chunk, units))));
+    if (din && dout) {
+        for (int64_t u0 = 0; u0 < units; u0 += chunk) {
+            const int nb = (int)std::min<int64_t>(chunk, units - u0);
+            SPTB_TRY(body(in, n, u0, out, n, u0, nb, pow2_at_least(nb)));
+        }
+        return SPTB_OK;
+    }
+    SPTB_TRY(ensure_pipe(p));
+    const size_t sbi = slice_bytes(in_fmt, in_len), sbo = slice_bytes(out_fmt, out_len);
+    SPTB_CUDA(cudaEventRecord(p->ev_start, p->stream));  // after earlier work on the plan stream
+    SPTB_CUDA(cudaStreamWaitEvent(p->io_in, p->ev_start, 0));
+    int64_t i = 0;
+    for (int64_t u0 = 0; u0 < units; u0 += chunk, ++i) {
+        const int k = (int)(i % sptb_plan::NPIPE);
+        const int nb = (int)std::min<int64_t>(chunk, units - u0);
         int64_t first, cnt;
         slice_range(in_fmt, n, u0, nb, &first, &cnt);
         const void* src = in;
         int64_t n_loc = n, u_loc = u0;
         if (!din) {
-            const size_t sb = slice_bytes(in_fmt, in_len);
-            SPTB_TRY(ensure_stage(&p->stage_in, &p->stage_in_bytes, sb * cnt));
-            SPTB_CUDA(cudaMemcpyAsync(p->stage_in, (const char*)in + sb * first, sb * cnt,
-                                      cudaMemcpyHostToDevice, p->stream));
-            src = p->stage_in;
-            n_loc = (in_fmt & SPTB_FMT_COMPLEX) ? cnt : cnt;
+            SPTB_TRY(ensure_stage(&p->pin[k], &p->pin_bytes[k], sbi * cnt));
+            if (i >= sptb_plan::NPIPE) SPTB_CUDA(cudaStreamWaitEvent(p->io_in, p->ev_comp[k], 0));
+            SPTB_CUDA(cudaMemcpyAsync(p->pin[k], (const char*)in + sbi * first, sbi * cnt,
+                                      cudaMemcpyHostToDevice, p->io_in));
+            SPTB_CUDA(cudaEventRecord(p->ev_in[k], p->io_in));
+            SPTB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_in[k], 0));
+            src = p->pin[k];
+            n_loc = cnt;
             u_loc = 0;
         }
         void* dst = out;
         int64_t on_loc = n, ou_loc = u0;
         if (!dout) {
-            const size_t sb = slice_bytes(out_fmt, out_len);
-            SPTB_TRY(ensure_stage(&p->stage_out, &p->stage_out_bytes, sb * cnt));
-            dst = p->stage_out;
+            SPTB_TRY(ensure_stage(&p->pout[k], &p->pout_bytes[k], sbo * cnt));
+            if (i >= sptb_plan::NPIPE) SPTB_CUDA(cudaStreamWaitEvent(p->stream, p->ev_out[k], 0));
+            dst = p->pout[k];
             on_loc = cnt;
             ou_loc = 0;
         }
-        SPTB_TRY(body(src, n_loc, u_loc, dst, on_loc, ou_loc, nb, B));
+        SPTB_TRY(body(src, n_loc, u_loc, dst, on_loc, ou_loc, nb, pow2_at_least(nb)));
+        SPTB_CUDA(cudaEventRecord(p->ev_comp[k], p->stream));
         if (!dout) {
-            const size_t sb = slice_bytes(out_fmt, out_len);
-            SPTB_CUDA(cudaMemcpyAsync((char*)out + sb * first, p->stage_out, sb * cnt,
-                                      cudaMemcpyDeviceToHost, p->stream));
+            SPTB_CUDA(cudaStreamWaitEvent(p->io_out, p->ev_comp[k], 0));
+            SPTB_CUDA(cudaMemcpyAsync((char*)out + sbo * first, p->pout[k], sbo * cnt,
+                                      cudaMemcpyDeviceToHost, p->io_out));
+            SPTB_CUDA(cudaEventRecord(p->ev_out[k], p->io_out));
         }
     }
-    if (!dout || !din) SPTB_CUDA(cudaStreamSynchronize(p->stream));
+    SPTB_CUDA(cudaStreamSynchronize(p->stream));
+    SPTB_CUDA(cudaStreamSynchronize(p->io_out));
+    SPTB_CUDA(cudaStreamSynchronize(p->io_in));
     return SPTB_OK;
 }
 
@@ -202,7 +241,7 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
     SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
     const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-    SPTB_TRY(launch_spmm<R>(s_permuted(p), vals, p->S1, p->G0, B, true, nullptr, st));
+    SPTB_TRY(launch_spmm_s<R>(p, vals, p->S1, p->G0, B, st));
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_INVERSE));
     return launch_unpack<R>(p->G0, p->M, p->deapo, scale / p->P, out, out_fmt, on, ou0, nb, st);
 }
@@ -306,9 +345,20 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
                     p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
-                    p->shp.s_colp, p->shp.sval};
+                    p->shp.s_colp, p->shp.sval, p->stl.tile_chunk, p->stl.chunks,
+                    p->stl.samp, p->stl.meta, p->stl.swval};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    for (int k = 0; k < sptb_plan::NPIPE; ++k) {
+        if (p->pin[k]) cudaFree(p->pin[k]);
+        if (p->pout[k]) cudaFree(p->pout[k]);
+        if (p->ev_in[k]) cudaEventDestroy(p->ev_in[k]);
+        if (p->ev_comp[k]) cudaEventDestroy(p->ev_comp[k]);
+        if (p->ev_out[k]) cudaEventDestroy(p->ev_out[k]);
+    }
+    if (p->ev_start) cudaEventDestroy(p->ev_start);
+    if (p->io_in) cudaStreamDestroy(p->io_in);
+    if (p->io_out) cudaStreamDestroy(p->io_out);
     for (void* b : p->extra)
         if (b) cudaFree(b);
     delete p;

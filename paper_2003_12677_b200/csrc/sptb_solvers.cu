@@ -1043,7 +1043,7 @@ struct Solver {
         FFTPlans* f;
         SPTB_TRY(get_fft(p, B, &f));
         const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-        SPTB_TRY(launch_spmm<R>(s_permuted(p), vals, rh, W, B, true, nullptr, st));
+        SPTB_TRY(launch_spmm_s<R>(p, vals, rh, W, B, st));
         return fft(f->fft2, W, CUFFT_INVERSE);
     }
 

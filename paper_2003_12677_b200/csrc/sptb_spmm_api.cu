@@ -184,7 +184,7 @@ int time_spmm(sptb_plan* p, int which, int B, int reps, double* ms) {
     SPTB_LAUNCHED();
     auto launch = [&]() -> int {
         if (adjoint) return launch_spmm_sh_patch<R>(p, x, y, B, nullptr, p->stream);
-        return launch_spmm<R>(s_permuted(p), vals, x, y, B, true, nullptr, p->stream);
+        return launch_spmm_s<R>(p, vals, x, y, B, p->stream);
     };
     for (int w = 0; w < 2; ++w) SPTB_TRY(launch());
     cudaEvent_t e0, e1;
