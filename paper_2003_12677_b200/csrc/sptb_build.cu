@@ -418,32 +418,49 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         }
     }
     sp.n_reg = sp.slot_mode ? cnt[npatch] : N;
+    std::vector<int> cls_start;  // slot mode: per patch, s' start of each border class (+ end)
     if (sp.slot_mode) {
-        // within a patch, alternate rows whose block origin has even and odd x:
-        // two rows sharing a half-warp then read cells of opposite parity, which
-        // keeps the box reads of the TMA kernel (even plane stride) conflict free
-        std::vector<int> ev, od;
+        // within a patch: border class (TL, T, TR, R, BR, B, BL, L, interior),
+        // then stencil-centre cell, then sample.  Every neighbour of the patch
+        // then finds the samples it shares with this patch (an edge column/row
+        // or a corner) in at most two contiguous s' runs, and the samples of
+        // one centre cell are contiguous (sptb_stile.cu stages runs by bulk copy)
+        cls_start.assign((size_t)npatch * STILE_NCLS1, 0);
+        std::vector<std::pair<uint64_t, int>> key;
         for (int64_t q = 0; q < npatch; ++q) {
-            ev.clear();
-            od.clear();
-            for (int64_t r = cnt[q]; r < cnt[q + 1]; ++r) (cx[order[r]] & 1 ? od : ev).push_back(order[r]);
-            size_t ie = 0, io = 0;
+            key.clear();
+            const int px = (int)(q % sp.npx), py = (int)(q / sp.npx);
             for (int64_t r = cnt[q]; r < cnt[q + 1]; ++r) {
-                const bool take_even = (ie < ev.size()) && ((r - cnt[q]) % 2 == 0 || io >= od.size());
-                const int s = take_even ? ev[ie++] : od[io++];
-                order[r] = s;
-                perm[s] = (int)r;
+                const int sm = order[r];
+                const int lx = cx[sm] - PATCH_W * px - 1, ly = cy[sm] - PATCH_W * py;
+                const int c = stile_class(lx, ly);
+                key.push_back({((uint64_t)c << 40) | ((uint64_t)(ly * PATCH_W + lx) << 32) | (uint64_t)sm, sm});
             }
+            std::sort(key.begin(), key.end());
+            int64_t r = cnt[q];
+            for (int c = 0; c < STILE_NCLS1; ++c) cls_start[q * STILE_NCLS1 + c] = (int)cnt[q + 1];
+            for (auto& kv : key) {
+                const int c = (int)(kv.first >> 40);
+                if (cls_start[q * STILE_NCLS1 + c] > r) cls_start[q * STILE_NCLS1 + c] = (int)r;
+                order[r] = kv.second;
+                perm[kv.second] = (int)r;
+                ++r;
+            }
+            // empty classes start where the next non-empty one does
+            for (int c = STILE_NCLS1 - 2; c >= 0; --c)
+                cls_start[q * STILE_NCLS1 + c] =
+                    std::min(cls_start[q * STILE_NCLS1 + c], cls_start[q * STILE_NCLS1 + c + 1]);
         }
     }
     std::vector<int4> items;
-    std::vector<int> rpn, emap, slot_src;
+    std::vector<unsigned char> item_perm;
+    std::vector<int> rpn, emap, slot_src, base_r;
     std::vector<unsigned> cell;
     if (sp.slot_mode) {
         // slot rows for every sample (irregular rows too: the output-tiled S
         // reads them; their base is unused)
         slot_src.assign((size_t)std::max<int64_t>(N, 1) * SLOT_STRIDE, -1);
-        std::vector<int> base_r(std::max<int64_t>(N, 1), 0);
+        base_r.assign(std::max<int64_t>(N, 1), 0);
         for (int64_t r = 0; r < N; ++r) {
             const int s = order[r];
             base_r[r] = base[s];
@@ -459,6 +476,22 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         // form the tail; spatial order is kept within both groups (L2 reuse of halos)
         std::stable_partition(items.begin(), items.end(),
                               [](const int4& it) { return it.z - it.y == PATCH_ITEM_ROWS; });
+        // per item, the order in which its rows are handed to lane groups: rows
+        // whose block origins differ in x parity alternate, so the two rows of a
+        // half-warp read cells of opposite parity (conflict-free box reads in
+        // the TMA kernel, whose plane stride is even)
+        item_perm.assign(items.size() * PATCH_ITEM_ROWS, 0);
+        std::vector<int> ev, od;
+        for (size_t it = 0; it < items.size(); ++it) {
+            ev.clear();
+            od.clear();
+            for (int r = items[it].y; r < items[it].z; ++r) ((base_r[r] & 1) ? od : ev).push_back(r - items[it].y);
+            size_t ie = 0, io = 0;
+            for (int k = 0; k < items[it].z - items[it].y; ++k) {
+                const bool take_even = ie < ev.size() && (k % 2 == 0 || io >= od.size());
+                item_perm[it * PATCH_ITEM_ROWS + k] = (unsigned char)(take_even ? ev[ie++] : od[io++]);
+            }
+        }
         int *dsrc = nullptr, *dbase = nullptr;
         SPTB_CUDA(cudaMalloc(&dsrc, sizeof(int) * slot_src.size()));
         SPTB_CUDA(cudaMalloc(&dbase, sizeof(int) * base_r.size()));
@@ -510,6 +543,10 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     SPTB_CUDA(cudaMalloc(&sp.s_colp, sizeof(int) * std::max<int64_t>(nnz, 1)));
     if (!items.empty())
         SPTB_CUDA(cudaMemcpy(sp.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+    if (!item_perm.empty()) {
+        SPTB_CUDA(cudaMalloc(&sp.item_perm, item_perm.size()));
+        SPTB_CUDA(cudaMemcpy(sp.item_perm, item_perm.data(), item_perm.size(), cudaMemcpyHostToDevice));
+    }
     SPTB_CUDA(cudaMemcpy(sp.perm, perm.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
     SPTB_CUDA(cudaMemcpy(sp.order, order.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
     if (!sp.slot_mode) {
@@ -539,7 +576,7 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         SPTB_LAUNCHED();
     }
     SPTB_CUDA(cudaStreamSynchronize(p->stream));
-    if (sp.slot_mode) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order));
+    if (sp.slot_mode) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order, cnt, cls_start));
     return SPTB_OK;
 }
 

@@ -111,28 +111,48 @@ struct PatchSH {
     int4* items = nullptr;    // {patch id, row begin (s'), row end, entry begin}
     int* rp = nullptr;        // N + 1, row pointers in s' order (record mode)
     void* meta = nullptr;     // nnz records {u32 cell, u32 pad, complex val} (record mode)
-    void* sval = nullptr;     // slot mode: [n_reg][SLOT_STRIDE] complex, slot 9 .x = base cell bits
+    void* sval = nullptr;     // slot mode: [N][SLOT_STRIDE] complex, slot 9 .x = base cell bits
+    unsigned char* item_perm = nullptr;  // slot mode: [n_items][PATCH_ITEM_ROWS] row hand-out order
     int* perm = nullptr;      // perm[s] = s'
     int* order = nullptr;     // order[s'] = s
     int* s_colp = nullptr;    // S column indices renumbered to s'
 };
 
-// S (grid <- samples) by 8x8 output tiles: a tile lists the samples whose
-// 3x3 block touches it (ascending s', in chunks of <= STILE_CHUNK), and per
-// chunk a metadata block of u32: 65 cell pointers (relative to the entry
-// start) followed by entries (local << 16 | local * 10 + slot), padded to 16 B.
-// Values come from the slot rows (conj(S^H) = S), unfiltered or w-folded.
+// S (grid <- samples) by output tiles = the 8x8 cells of a sample patch.  A
+// tile needs the samples centred in its 10x10 centre box: its own patch and
+// an edge column/row or corner of each neighbour -- at most STILE_RUNS
+// contiguous s' runs thanks to the border-class order of build_patches.  The
+// staged runs are indexed by a centre table: for each box cell, the (begin,
+// count) of its samples in the staged list.  Tiles with more than STILE_CAP
+// samples (the dense centre) use a CSR gather; cells touched by irregular
+// samples get a deterministic fix-up pass.
 constexpr int STILE = 8;
-constexpr int STILE_CHUNK = 128;
+constexpr int STILE_RUNS = 10;
+constexpr int STILE_CAP = 192;
+constexpr int STILE_NCLS1 = 10;  // 9 border classes + end
+inline int stile_class(int lx, int ly) {  // TL T TR R BR B BL L interior
+    const bool l = lx == 0, r = lx == PATCH_W - 1, t = ly == 0, b = ly == PATCH_W - 1;
+    if (t) return l ? 0 : (r ? 2 : 1);
+    if (b) return r ? 4 : (l ? 6 : 5);
+    if (r) return 3;
+    if (l) return 7;
+    return 8;
+}
+struct alignas(16) STileMeta {
+    int2 run[STILE_RUNS];        // {s' begin, count}
+    unsigned table[100];         // centre box cell -> begin | count << 16 (staged list)
+    int ns, pad0, pad1, pad2;
+};
 
 struct STiles {
-    int ntx = 0, nty = 0;
-    int64_t n_chunks = 0;
-    int* tile_chunk = nullptr;   // ntiles + 1 chunk offsets
-    int4* chunks = nullptr;      // {tile, sample begin, n samples, meta offset (u32 units)}
-    int* samp = nullptr;         // s' lists
-    unsigned* meta = nullptr;
-    int max_meta = 0;            // largest metadata block (u32 units)
+    int n_sparse = 0, n_dense = 0;
+    int* sparse = nullptr;       // tile (= patch) ids for the staged kernel
+    int* dense = nullptr;        // tile ids for the CSR-gather kernel
+    STileMeta* meta = nullptr;   // per patch
+    int n_fix = 0;               // cells touched by irregular samples (outside dense tiles)
+    int* fix_cell = nullptr;     // grid cell m
+    int* fix_ptr = nullptr;      // n_fix + 1
+    int2* fix_ent = nullptr;     // {s', slot}
     void* swval = nullptr;       // slot rows with the filter folded (w[s] * sval)
 };
 
@@ -237,7 +257,8 @@ template <typename R>
 int launch_spmm_s(const sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B,
                   cudaStream_t st);
 int build_stiles(sptb_plan* p, const std::vector<int>& cx, const std::vector<int>& cy,
-                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order);
+                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order,
+                 const std::vector<int64_t>& cnt, const std::vector<int>& cls_start);
 int fold_slot_filter(sptb_plan* p);
 // S with columns renumbered to the patch order s'
 inline DevCSR s_permuted(const sptb_plan* p) {

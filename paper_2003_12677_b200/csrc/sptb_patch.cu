@@ -435,6 +435,7 @@ k_sh_rows(const int* __restrict__ order, const int* __restrict__ rp, const int* 
 // half-warp: their cells differ in parity, which makes the 16 reads of a
 // half-warp hit 16 distinct 8-byte bank pairs.
 // ---------------------------------------------------------------------------
+static_assert(PATCH_ITEM_ROWS % 16 == 0 && PATCH_ITEM_ROWS <= 256, "item rows: u8 hand-out order, 16-byte copies");
 constexpr int TMA_BY = SLOT_BW + 1;             // box rows (one spare)
 constexpr int TMA_PS = SLOT_BW * TMA_BY;        // plane stride in cells
 
@@ -448,7 +449,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 template <typename R, int G, int CPL, bool SUB>
 __global__ void __launch_bounds__(PT, 4)
 k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ items,
-         const typename PCplx<R>::T* __restrict__ sval, int npx,
+         const unsigned char* __restrict__ item_perm, const typename PCplx<R>::T* __restrict__ sval, int npx,
          typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub) {
     using C = typename PCplx<R>::T;
     constexpr int BB = G * CPL, NG = PT / G;
@@ -457,6 +458,7 @@ k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ item
     __shared__ __align__(8) unsigned long long bar;
     const C* xs = reinterpret_cast<const C*>(smem_raw);
     const C* rows = reinterpret_cast<const C*>(smem_raw + XS_BYTES);
+    const unsigned char* sperm = smem_raw + XS_BYTES + PATCH_ITEM_ROWS * SLOT_STRIDE * (int)sizeof(C);
     const int tid = threadIdx.x;
     const int4 d = items[blockIdx.x];
     const int r0 = d.y, nr = d.z - d.y;
@@ -467,7 +469,7 @@ k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ item
         const unsigned box_bytes = BB * TMA_PS * (unsigned)sizeof(C);
         const unsigned row_bytes = (unsigned)(nr * SLOT_STRIDE * (int)sizeof(C));
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sbar),
-                     "r"(box_bytes + row_bytes) : "memory");
+                     "r"(box_bytes + row_bytes + PATCH_ITEM_ROWS) : "memory");
         const int bx0 = (d.x % npx) * PATCH_W, by0 = (d.x / npx) * PATCH_W - 1;  // slot-mode patch origin
         const int ex = (int)sizeof(C) / 8;  // 8-byte tensor elements per complex
         asm volatile(
@@ -480,12 +482,18 @@ k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ item
                 (unsigned)__cvta_generic_to_shared(smem_raw + XS_BYTES)),
             "l"(sval + (size_t)r0 * SLOT_STRIDE), "r"(row_bytes), "r"(sbar)
             : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                (unsigned)__cvta_generic_to_shared(sperm)),
+            "l"(item_perm + (size_t)blockIdx.x * PATCH_ITEM_ROWS), "r"(PATCH_ITEM_ROWS), "r"(sbar)
+            : "memory");
     }
     __syncthreads();
     mbar_wait(sbar, 0);
 
     const int g = tid / G, lig = tid % G;
-    for (int r = g; r < nr; r += NG) {
+    for (int rr = g; rr < nr; rr += NG) {
+        const int r = sperm[rr];
         const C* rv = rows + r * SLOT_STRIDE;
         C acc[CPL];
         if constexpr (sizeof(C) == 8) {
@@ -567,7 +575,7 @@ static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const voi
     const PatchSH& sp = p->shp;
     constexpr int BB = G * CPL;
     constexpr int XS_BYTES = (BB * TMA_PS * (int)sizeof(C) + 127) & ~127;
-    const size_t sm = XS_BYTES + (size_t)PATCH_ITEM_ROWS * SLOT_STRIDE * sizeof(C);
+    const size_t sm = XS_BYTES + (size_t)PATCH_ITEM_ROWS * SLOT_STRIDE * sizeof(C) + PATCH_ITEM_ROWS;
     if (sp.n_items > 0) {
         const int ex = (int)sizeof(C) / 8;
         CUtensorMap tm;
@@ -583,8 +591,8 @@ static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const voi
         auto run = [&](auto kern) -> int {
             SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            kern<<<(unsigned)sp.n_items, PT, sm, st>>>(tm, sp.items, (const C*)sp.sval, sp.npx, (C*)y,
-                                                       (const C*)sub);
+            kern<<<(unsigned)sp.n_items, PT, sm, st>>>(tm, sp.items, sp.item_perm, (const C*)sp.sval, sp.npx,
+                                                       (C*)y, (const C*)sub);
             SPTB_LAUNCHED();
             return SPTB_OK;
         };

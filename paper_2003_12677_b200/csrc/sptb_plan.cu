@@ -345,8 +345,9 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
                     p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
-                    p->shp.s_colp, p->shp.sval, p->stl.tile_chunk, p->stl.chunks,
-                    p->stl.samp, p->stl.meta, p->stl.swval};
+                    p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->stl.sparse,
+                    p->stl.dense, p->stl.meta, p->stl.fix_cell, p->stl.fix_ptr, p->stl.fix_ent,
+                    p->stl.swval};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int k = 0; k < sptb_plan::NPIPE; ++k) {

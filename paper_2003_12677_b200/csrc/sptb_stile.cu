@@ -1,28 +1,28 @@
 // Output-tiled S SpMM (adjoint / gridrec direction):  Y[b][m] = S_(w) X,
 // X [s'][b] (batch innermost, the FFT1-side operand), Y batch-outer for the
-// inverse 2-D FFT.
+// inverse 2-D FFT.  The reference computes it with scipy CSR
+// (operators.py:124-136, 178-184).
 //
-// S = conj(S^H)^T, and every sample's nonzeros sit in the 3x3 block around its
-// stencil centre (gridding.py:104-143), so the nonzeros of an 8x8 tile of grid
-// cells come from the samples whose block touches the tile.  One CTA per tile:
-//   * cp.async stages, per needed sample, its X row (B complex, contiguous)
-//     and its slot row (9 values + base, the S^H slot layout of sptb_patch.cu),
-//     plus the chunk's u32 metadata (cell pointers, entries); per-row bulk
-//     (TMA) copies measured 3x slower here: ~150 requests of 80-256 B per tile;
-//   * a group of 16 lanes per grid cell accumulates conj(v) * X[s] over the
-//     cell's entries (lanes own batch columns 2*lig, 2*lig+1: LDS.128 of the
-//     staged row, conflict free); tiles touched by more than STILE_CHUNK samples
-//     loop over chunks, accumulating in registers (entry order is ascending
-//     (s', slot): deterministic and independent of the batch slot);
-//   * the 64 x B tile goes through shared memory and leaves as 64-byte row runs
-//     of each batch plane.  Tiles without samples write zeros (the grid outside
-//     the disk is part of the inverse FFT input).
-// The reference computes the same product with scipy CSR (operators.py:124-136,
-// 178-184); no per-nonzero column index or value is stored here: an entry is
-// 2 bytes (local sample, slot), the values are the slot rows shared with S^H.
+// S = conj(S^H)^T and every sample's nonzeros sit in the 3x3 block around its
+// stencil centre (gridding.py:104-143): grid cell m receives, from each sample
+// centred at m - (ex, ey) (ex, ey in {-1, 0, 1}), the conjugate of that
+// sample's slot (ey + 1) * 3 + (ex + 1).  A tile is the 8x8 cells of a sample
+// patch; its samples (own patch + neighbour edge columns/rows/corners) are at
+// most STILE_RUNS contiguous s' runs (border-class order, build_patches):
+//   * one elected thread stages the runs -- X rows and slot rows -- and the
+//     tile's centre table with <= 21 bulk copies on one mbarrier;
+//   * a group of 16 lanes per cell walks the 9 neighbour centres; per sample
+//     it reads one broadcast slot value (compile-time slot index) and one
+//     16-byte piece of the sample's X row -- no per-nonzero index at all;
+//   * the 64 x B tile leaves through shared memory as row runs per plane.
+// Dense tiles (> STILE_CAP samples, the centre of the polar grid) gather
+// through the CSR of S instead; cells touched by irregular samples (stencil
+// centre outside the grid) get a deterministic fix-up pass.  Accumulation
+// order is fixed (neighbour, then s'): results do not depend on the batch slot.
 #include "sptb_internal.cuh"
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 namespace sptb {
@@ -36,79 +36,110 @@ template <> struct TCplx<double> { using T = double2; };
 constexpr int TT = 256;  // threads per CTA
 constexpr int TG = 16;   // lanes per grid cell
 
-__device__ __forceinline__ void tcp16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem));
+__device__ __forceinline__ void sbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "SW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra SW;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void sbulk(void* dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
 }
 
-// BB batch columns; lane lig of a cell group owns columns [CW*lig, CW*lig+CW)
+// tile (64 cells x BB planes) -> y: cells (8px + 1 + ox, 8py + oy); the x = 0
+// column (no S entries: border, gridding.py:136-137) is written as zeros by
+// the px = 0 tiles
+template <typename C, int BB>
+__device__ __forceinline__ void store_tile(const C* ot, int px, int py, int X, int Y, long long M, C* y) {
+    constexpr int OS = STILE * STILE + 1;
+    for (int e = threadIdx.x; e < BB * STILE * STILE; e += TT) {
+        const int b = e / (STILE * STILE), cell = e % (STILE * STILE);
+        const int gx = STILE * px + 1 + cell % STILE, gy = STILE * py + cell / STILE;
+        if (gx < X && gy < Y) y[(size_t)b * M + (size_t)gy * X + gx] = ot[b * OS + cell];
+    }
+    if (px == 0)
+        for (int e = threadIdx.x; e < BB * STILE; e += TT) {
+            const int b = e / STILE, gy = STILE * py + e % STILE;
+            if (gy < Y) {
+                C z;
+                z.x = z.y = 0;
+                y[(size_t)b * M + (size_t)gy * X] = z;
+            }
+        }
+}
+
 template <typename R, int BB>
 __global__ void __launch_bounds__(TT)
-k_s_tile(const int* __restrict__ tile_chunk, const int4* __restrict__ chunks,
-         const int* __restrict__ samp, const unsigned* __restrict__ meta,
-         const typename TCplx<R>::T* __restrict__ vals, int ntx, int X, int Y, long long M,
-         const typename TCplx<R>::T* __restrict__ x, typename TCplx<R>::T* __restrict__ y) {
+k_s_tile(const int* __restrict__ tiles, const STileMeta* __restrict__ meta, int npx, int X, int Y,
+         long long M, const typename TCplx<R>::T* __restrict__ x,
+         const typename TCplx<R>::T* __restrict__ vals, typename TCplx<R>::T* __restrict__ y) {
     using C = typename TCplx<R>::T;
-    constexpr int CW = BB >= 2 * TG ? BB / TG : 1;    // columns per lane
-    constexpr int NL = BB / CW;                       // lanes per cell actually used
-    constexpr int NGRP = TT / TG;                     // cell groups per CTA
-    constexpr int CPG = STILE * STILE / NGRP;         // cells per group
-    constexpr int XROW = BB * (int)sizeof(C);         // staged X row bytes (power of two)
+    constexpr int CW = BB >= 2 * TG ? BB / TG : 1;  // columns per lane
+    constexpr int NL = BB / CW;                     // lanes per cell in use
+    constexpr int NGRP = TT / TG;
+    constexpr int CPG = STILE * STILE / NGRP;       // cells per group
+    constexpr int XROW = BB * (int)sizeof(C);
     constexpr int VROW = SLOT_STRIDE * (int)sizeof(C);
-    constexpr int UX = XROW / 16, UV = VROW / 16, US = UX + UV;  // 16-byte units per sample
-    constexpr int NW = TT / 32;
+    constexpr int OS = STILE * STILE + 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ int s_ids[STILE_CHUNK];
-    unsigned char* xs = smem_raw;                                   // [CHUNK][BB] C
-    unsigned char* vs = xs + STILE_CHUNK * XROW;                    // [CHUNK][10] C
-    unsigned* ms = reinterpret_cast<unsigned*>(vs + STILE_CHUNK * VROW);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tile = blockIdx.x;
-    const int c0 = tile_chunk[tile], c1 = tile_chunk[tile + 1];
-    const int g = tid / TG, lig = tid % TG;
+    __shared__ __align__(16) unsigned tab[100];
+    __shared__ __align__(8) unsigned long long bar;
+    unsigned char* xs = smem_raw;                       // [CAP][BB] C
+    unsigned char* vs = xs + STILE_CAP * XROW;          // [CAP][10] C
+    const int tid = threadIdx.x;
+    const int tile = tiles[blockIdx.x];
+    const int px = tile % npx, py = tile / npx;
+    const STileMeta* mt = meta + tile;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        const int ns = mt->ns;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"((unsigned)ns * (XROW + VROW) + 400u) : "memory");
+        sbulk(tab, mt->table, 400u, sb);
+        int off = 0;
+#pragma unroll 1
+        for (int i = 0; i < STILE_RUNS; ++i) {
+            const int2 rn = mt->run[i];
+            if (rn.y > 0) {
+                sbulk(xs + off * XROW, x + (size_t)rn.x * BB, (unsigned)(rn.y * XROW), sb);
+                sbulk(vs + off * VROW, vals + (size_t)rn.x * SLOT_STRIDE, (unsigned)(rn.y * VROW), sb);
+                off += rn.y;
+            }
+        }
+    }
+    __syncthreads();
+    sbar_wait(sb, 0);
 
-    // accumulators: acc += v * x split as (vr * x) and (vi * x), conj applied at the end
+    const int g = tid / TG, lig = tid % TG;
     C ar[CPG][CW], ai[CPG][CW];
 #pragma unroll
     for (int j = 0; j < CPG; ++j)
 #pragma unroll
         for (int w = 0; w < CW; ++w) ar[j][w].x = ar[j][w].y = ai[j][w].x = ai[j][w].y = 0;
-
-    for (int c = c0; c < c1; ++c) {
-        const int4 ch = chunks[c];  // {tile, sample begin, n samples, meta offset (u32 units)}
-        const int ns = ch.z;
-        const unsigned* mg = meta + ch.w;
-        // stage: a warp per sample, lane u < US copies 16-byte unit u of the
-        // sample's X row (u < UX) or slot row; then the metadata block
-        if (tid < ns) s_ids[tid] = samp[ch.y + tid];
-        __syncthreads();
-        for (int i = warp; i < ns; i += NW) {
-            const long long sm = s_ids[i];
-            if (lane < UX)
-                tcp16(xs + i * XROW + 16 * lane, reinterpret_cast<const char*>(x + sm * BB) + 16 * lane);
-            else if (lane < US)
-                tcp16(vs + i * VROW + 16 * (lane - UX),
-                      reinterpret_cast<const char*>(vals + sm * SLOT_STRIDE) + 16 * (lane - UX));
-        }
-        const int mu = (((int)__ldg(mg + STILE * STILE) + STILE * STILE + 1 + 3) & ~3) / 4;
-        for (int u = tid; u < mu; u += TT) tcp16(ms + 4 * u, mg + 4 * u);
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();
-
-        if (lig < NL) {
-            const unsigned char* xl = xs + lig * CW * (int)sizeof(C);
-            const unsigned* ent = ms + STILE * STILE + 1;
+    if (lig < NL) {
+        const unsigned char* xl = xs + lig * CW * (int)sizeof(C);
 #pragma unroll
-            for (int j = 0; j < CPG; ++j) {
-                const int cell = g + NGRP * j;
-                const int e0 = ms[cell], e1 = ms[cell + 1];
-#pragma unroll 4
-                for (int e = e0; e < e1; ++e) {
-                    const unsigned rec = ent[e];  // (local sample << 16) | (local * 10 + slot)
-                    const C v = reinterpret_cast<const C*>(vs)[rec & 0xffffu];
-                    const C* xp = reinterpret_cast<const C*>(xl + (rec >> 16) * XROW);
+        for (int j = 0; j < CPG; ++j) {
+            const int cell = g + NGRP * j;
+            const int bx = cell % STILE + 1, by = cell / STILE + 1;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int ey = k / 3 - 1, ex = k % 3 - 1;
+                const unsigned t = tab[(by - ey) * 10 + (bx - ex)];
+                const int beg = (int)(t & 0xffffu), cnt = (int)(t >> 16);
+                const C* vp = reinterpret_cast<const C*>(vs) + beg * SLOT_STRIDE + k;
+                const unsigned char* xp = xl + beg * XROW;
+#pragma unroll 2
+                for (int i = 0; i < cnt; ++i) {
+                    const C v = vp[i * SLOT_STRIDE];
                     if constexpr (sizeof(C) == 8 && CW == 2) {
-                        const float4 xv = *reinterpret_cast<const float4*>(xp);
+                        const float4 xv = *reinterpret_cast<const float4*>(xp + i * XROW);
                         const float2 x0 = make_float2(xv.x, xv.y), x1 = make_float2(xv.z, xv.w);
                         float2 r0 = make_float2(ar[j][0].x, ar[j][0].y), r1 = make_float2(ar[j][1].x, ar[j][1].y);
                         float2 i0 = make_float2(ai[j][0].x, ai[j][0].y), i1 = make_float2(ai[j][1].x, ai[j][1].y);
@@ -119,9 +150,10 @@ k_s_tile(const int* __restrict__ tile_chunk, const int4* __restrict__ chunks,
                         ar[j][0].x = r0.x; ar[j][0].y = r0.y; ar[j][1].x = r1.x; ar[j][1].y = r1.y;
                         ai[j][0].x = i0.x; ai[j][0].y = i0.y; ai[j][1].x = i1.x; ai[j][1].y = i1.y;
                     } else {
+                        const C* xq = reinterpret_cast<const C*>(xp + i * XROW);
 #pragma unroll
                         for (int w = 0; w < CW; ++w) {
-                            const C xv = xp[w];
+                            const C xv = xq[w];
                             ar[j][w].x = fma(v.x, xv.x, ar[j][w].x);
                             ar[j][w].y = fma(v.x, xv.y, ar[j][w].y);
                             ai[j][w].x = fma(v.y, xv.x, ai[j][w].x);
@@ -131,40 +163,100 @@ k_s_tile(const int* __restrict__ tile_chunk, const int4* __restrict__ chunks,
                 }
             }
         }
-        __syncthreads();  // the stage is refilled by the next chunk
     }
-
-    // conj(v) * x = (vr xr + vi xi, vr xi - vi xr); tile -> shared [b][65]
+    __syncthreads();  // the staging area becomes the output tile
     C* ot = reinterpret_cast<C*>(smem_raw);
-    constexpr int OS = STILE * STILE + 1;
     if (lig < NL) {
 #pragma unroll
         for (int j = 0; j < CPG; ++j)
 #pragma unroll
             for (int w = 0; w < CW; ++w) {
-                C o;
+                C o;  // conj(v) x = (vr xr + vi xi, vr xi - vi xr)
                 o.x = ar[j][w].x + ai[j][w].y;
                 o.y = ar[j][w].y - ai[j][w].x;
                 ot[(lig * CW + w) * OS + g + NGRP * j] = o;
             }
     }
     __syncthreads();
-    // cell pairs: thread -> (pair p = tid % 32, plane b = tid / 32 + 8 k)
-    const int tx0 = (tile % ntx) * STILE, ty0 = (tile / ntx) * STILE;
-    const int pr = tid & 31;
-    const int cell = 2 * pr, gx = tx0 + cell % STILE, gy = ty0 + cell / STILE;
-    if (gy < Y) {
-        C* yo = y + (size_t)gy * X + gx;
+    store_tile<C, BB>(ot, px, py, X, Y, M, y);
+}
+
+// dense tiles: gather through the CSR of S (columns renumbered to s'); the
+// values are the ones of S itself (no conjugation)
+template <typename R, int BB>
+__global__ void __launch_bounds__(TT)
+k_s_dense(const int* __restrict__ tiles, int npx, int X, int Y, long long M, const int* __restrict__ rp,
+          const int* __restrict__ col, const typename TCplx<R>::T* __restrict__ val,
+          const typename TCplx<R>::T* __restrict__ x, typename TCplx<R>::T* __restrict__ y) {
+    using C = typename TCplx<R>::T;
+    constexpr int CW = BB >= 2 * TG ? BB / TG : 1;
+    constexpr int NL = BB / CW;
+    constexpr int NGRP = TT / TG;
+    constexpr int CPG = STILE * STILE / NGRP;
+    constexpr int OS = STILE * STILE + 1;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    C* ot = reinterpret_cast<C*>(smem_raw);
+    const int tile = tiles[blockIdx.x];
+    const int px = tile % npx, py = tile / npx;
+    const int g = threadIdx.x / TG, lig = threadIdx.x % TG;
+#pragma unroll 1
+    for (int j = 0; j < CPG; ++j) {
+        const int cell = g + NGRP * j;
+        const int gx = STILE * px + 1 + cell % STILE, gy = STILE * py + cell / STILE;
+        C a[CW];
+#pragma unroll
+        for (int w = 0; w < CW; ++w) a[w].x = a[w].y = 0;
+        if (gx < X && gy < Y && lig < NL) {
+            const long long m = (long long)gy * X + gx;
+            const int e0 = rp[m], e1 = rp[m + 1];
 #pragma unroll 4
-        for (int b = tid >> 5; b < BB; b += NW) {
-            const C v0 = ot[b * OS + cell], v1 = ot[b * OS + cell + 1];
-            if (gx + 1 < X) {
-                yo[(size_t)b * M] = v0;
-                yo[(size_t)b * M + 1] = v1;
-            } else if (gx < X) {
-                yo[(size_t)b * M] = v0;
+            for (int e = e0; e < e1; ++e) {
+                const C v = __ldg(val + e);
+                const C* xq = x + (size_t)__ldg(col + e) * BB + lig * CW;
+#pragma unroll
+                for (int w = 0; w < CW; ++w) {
+                    const C xv = __ldg(xq + w);
+                    a[w].x = fma(v.x, xv.x, a[w].x);
+                    a[w].x = fma(-v.y, xv.y, a[w].x);
+                    a[w].y = fma(v.x, xv.y, a[w].y);
+                    a[w].y = fma(v.y, xv.x, a[w].y);
+                }
             }
         }
+        if (lig < NL)
+#pragma unroll
+            for (int w = 0; w < CW; ++w) ot[(lig * CW + w) * OS + cell] = a[w];
+    }
+    __syncthreads();
+    store_tile<C, BB>(ot, px, py, X, Y, M, y);
+}
+
+// cells touched by irregular samples: y[b][m] += sum conj(slot value) x[s'][b]
+template <typename R>
+__global__ void k_s_fix(int n_fix, const int* __restrict__ cell, const int* __restrict__ ptr,
+                        const int2* __restrict__ ent, const typename TCplx<R>::T* __restrict__ vals, int B,
+                        long long M, const typename TCplx<R>::T* __restrict__ x,
+                        typename TCplx<R>::T* __restrict__ y) {
+    using C = typename TCplx<R>::T;
+    const long long n = (long long)n_fix * B;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / B), b = (int)(e % B);
+        C a;
+        a.x = a.y = 0;
+        for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+            const int2 t = ent[k];
+            const C v = vals[(size_t)t.x * SLOT_STRIDE + t.y], xv = x[(size_t)t.x * B + b];
+            a.x = fma(v.x, xv.x, a.x);
+            a.x = fma(v.y, xv.y, a.x);
+            a.y = fma(v.x, xv.y, a.y);
+            a.y = fma(-v.y, xv.x, a.y);
+        }
+        C* o = y + (size_t)b * M + cell[i];
+        C cur = *o;
+        cur.x += a.x;
+        cur.y += a.y;
+        *o = cur;
     }
 }
 
@@ -189,19 +281,34 @@ __global__ void k_fold_slots(const typename TCplx<R>::T* __restrict__ sval, cons
 }
 
 template <typename R, int BB>
-int s_tile_dispatch(const sptb_plan* p, const void* vals, const void* x, void* y, cudaStream_t st) {
+int s_tile_dispatch(const sptb_plan* p, const void* csr_vals, const void* slot, const void* x, void* y,
+                    cudaStream_t st) {
     using C = typename TCplx<R>::T;
     const STiles& t = p->stl;
-    const int ntiles = t.ntx * t.nty;
-    const size_t sm = (size_t)STILE_CHUNK * (BB + SLOT_STRIDE) * sizeof(C) + 4 * (size_t)t.max_meta + 16;
-    const size_t smo = (size_t)BB * (STILE * STILE + 1) * sizeof(C);
-    const size_t smt = std::max(sm, smo);
-    auto kern = k_s_tile<R, BB>;
-    SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
-    SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    kern<<<ntiles, TT, smt, st>>>(t.tile_chunk, t.chunks, t.samp, t.meta, (const C*)vals, t.ntx, p->X, p->Y,
-                                  p->M, (const C*)x, (C*)y);
-    SPTB_LAUNCHED();
+    const int npx = p->shp.npx;
+    const size_t so = (size_t)BB * (STILE * STILE + 1) * sizeof(C);
+    if (t.n_sparse > 0) {
+        const size_t sm = std::max((size_t)STILE_CAP * (BB + SLOT_STRIDE) * sizeof(C), so);
+        auto kern = k_s_tile<R, BB>;
+        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        kern<<<t.n_sparse, TT, sm, st>>>(t.sparse, t.meta, npx, p->X, p->Y, p->M, (const C*)x,
+                                        (const C*)slot, (C*)y);
+        SPTB_LAUNCHED();
+    }
+    if (t.n_dense > 0) {
+        auto kern = k_s_dense<R, BB>;
+        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so));
+        kern<<<t.n_dense, TT, so, st>>>(t.dense, npx, p->X, p->Y, p->M, p->S.row_ptr, p->shp.s_colp,
+                                       (const C*)csr_vals, (const C*)x, (C*)y);
+        SPTB_LAUNCHED();
+    }
+    if (t.n_fix > 0) {
+        const long long n = (long long)t.n_fix * BB;
+        k_s_fix<R><<<(unsigned)std::min<long long>((n + 255) / 256, 148LL * 8), 256, 0, st>>>(
+            t.n_fix, t.fix_cell, t.fix_ptr, t.fix_ent, (const C*)slot, BB, p->M, (const C*)x, (C*)y);
+        SPTB_LAUNCHED();
+    }
     return SPTB_OK;
 }
 
@@ -211,13 +318,15 @@ template <typename R>
 int launch_spmm_s(const sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B,
                   cudaStream_t st) {
     const void* slot = nullptr;
-    if (p->stl.tile_chunk && p->shp.sval) {
+    if (p->stl.meta && p->shp.sval) {
         if (vals == p->S.val) slot = p->shp.sval;
         else if (vals == p->SW_val && p->stl.swval) slot = p->stl.swval;
     }
     // bulk copies need 16-byte rows and a 16-byte aligned operand
-    const bool aligned = ((uintptr_t)x_sb % 16) == 0 && (size_t)B * p->csize >= 16;
-    // the tiled kernel is opt-in (SPTB_STILE=1) until it beats the row gather
+    const bool aligned = ((uintptr_t)x_sb % 16) == 0 && (size_t)B * p->csize >= 16 &&
+                         (size_t)STILE_CAP * (B + SLOT_STRIDE) * p->csize <= 200 * 1024;
+    // opt-in (SPTB_STILE=1) until it beats the row gather: the dense centre
+    // tiles still serialise
     static const bool use_tiles = [] {
         const char* e = getenv("SPTB_STILE");
         return e && e[0] == '1';
@@ -225,13 +334,13 @@ int launch_spmm_s(const sptb_plan* p, const void* vals, const void* x_sb, void* 
     if (!slot || !aligned || !use_tiles)
         return launch_spmm<R>(s_permuted(p), vals, x_sb, y_bm, B, true, nullptr, st);
     switch (B) {
-        case 1: return s_tile_dispatch<R, 1>(p, slot, x_sb, y_bm, st);
-        case 2: return s_tile_dispatch<R, 2>(p, slot, x_sb, y_bm, st);
-        case 4: return s_tile_dispatch<R, 4>(p, slot, x_sb, y_bm, st);
-        case 8: return s_tile_dispatch<R, 8>(p, slot, x_sb, y_bm, st);
-        case 16: return s_tile_dispatch<R, 16>(p, slot, x_sb, y_bm, st);
-        case 32: return s_tile_dispatch<R, 32>(p, slot, x_sb, y_bm, st);
-        case 64: return s_tile_dispatch<R, 64>(p, slot, x_sb, y_bm, st);
+        case 1: return s_tile_dispatch<R, 1>(p, vals, slot, x_sb, y_bm, st);
+        case 2: return s_tile_dispatch<R, 2>(p, vals, slot, x_sb, y_bm, st);
+        case 4: return s_tile_dispatch<R, 4>(p, vals, slot, x_sb, y_bm, st);
+        case 8: return s_tile_dispatch<R, 8>(p, vals, slot, x_sb, y_bm, st);
+        case 16: return s_tile_dispatch<R, 16>(p, vals, slot, x_sb, y_bm, st);
+        case 32: return s_tile_dispatch<R, 32>(p, vals, slot, x_sb, y_bm, st);
+        case 64: return s_tile_dispatch<R, 64>(p, vals, slot, x_sb, y_bm, st);
     }
     return fail(SPTB_ERR_ARG, "spmm: batch must be a power of two <= 64");
 }
@@ -260,99 +369,115 @@ int fold_slot_filter(sptb_plan* p) {
     return SPTB_OK;
 }
 
-// Host build of the tile lists (once per plan).  Entry (s', slot) of tile t
-// for grid cell m = (cy + ey) * X + (cx + ex), slot = (ey + 1) * 3 + (ex + 1).
+// Host build of the tile metadata (once per plan, slot mode).  Tile = sample
+// patch q = (px, py); staged runs in a fixed order; the centre table maps
+// the 10x10 centre box (x in [8px, 8px+9], y in [8py-1, 8py+8]) to the staged
+// list.
 int build_stiles(sptb_plan* p, const std::vector<int>& cx, const std::vector<int>& cy,
-                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order) {
+                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order,
+                 const std::vector<int64_t>& cnt, const std::vector<int>& cls_start) {
     STiles& t = p->stl;
-    const int X = p->X, Y = p->Y;
-    const int64_t N = p->N;
-    t.ntx = (X + STILE - 1) / STILE;
-    t.nty = (Y + STILE - 1) / STILE;
-    const int64_t ntiles = (int64_t)t.ntx * t.nty;
-    std::vector<int64_t> cnt(ntiles + 1, 0);
-    for (int64_t r = 0; r < N; ++r) {
-        const int s = order[r];
-        for (int k = rp[s]; k < rp[s + 1]; ++k) {
+    const PatchSH& sp = p->shp;
+    const int X = p->X, npx = sp.npx, npy = sp.npy;
+    const int64_t npatch = (int64_t)npx * npy;
+    std::vector<STileMeta> meta((size_t)npatch);
+    std::vector<int> sparse, dense;
+    std::vector<char> is_dense((size_t)npatch, 0);
+    auto cs = [&](int64_t q, int c) { return cls_start[(size_t)q * STILE_NCLS1 + c]; };
+    for (int64_t q = 0; q < npatch; ++q) {
+        STileMeta& m = meta[(size_t)q];
+        std::memset(&m, 0, sizeof(m));
+        const int px = (int)(q % npx), py = (int)(q / npx);
+        int nr = 0;
+        auto add = [&](int64_t b, int64_t e) {
+            if (e > b) m.run[nr++] = make_int2((int)b, (int)(e - b));
+        };
+        auto nb = [&](int dx, int dy, int c0, int c1) {
+            const int qx = px + dx, qy = py + dy;
+            if (qx < 0 || qx >= npx || qy < 0 || qy >= npy) return;
+            const int64_t qq = (int64_t)qy * npx + qx;
+            add(cs(qq, c0), cs(qq, c1));
+        };
+        add(cnt[q], cnt[q + 1]);   // own patch
+        nb(-1, 0, 2, 5);           // left: TR R BR
+        nb(1, 0, 0, 1);            // right: TL ...
+        nb(1, 0, 6, 8);            //        ... BL L
+        nb(0, -1, 4, 7);           // top: BR B BL
+        nb(0, 1, 0, 3);            // bottom: TL T TR
+        nb(-1, -1, 4, 5);          // top-left: BR
+        nb(1, -1, 6, 7);           // top-right: BL
+        nb(-1, 1, 2, 3);           // bottom-left: TR
+        nb(1, 1, 0, 1);            // bottom-right: TL
+        int ns = 0;
+        for (int i = 0; i < nr; ++i) ns += m.run[i].y;
+        m.ns = ns;
+        if (ns > STILE_CAP) {
+            is_dense[(size_t)q] = 1;
+            dense.push_back((int)q);
+            continue;
+        }
+        sparse.push_back((int)q);
+        int li = 0, last = -1;
+        for (int i = 0; i < nr; ++i)
+            for (int r = m.run[i].x; r < m.run[i].x + m.run[i].y; ++r, ++li) {
+                const int smp = order[r];
+                const int bx = cx[smp] - STILE * px, by = cy[smp] - (STILE * py - 1);
+                if (bx < 0 || bx > 9 || by < 0 || by > 9)
+                    return fail(SPTB_ERR_STATE, "tile build: sample centre outside the tile's centre box");
+                const int n = by * 10 + bx;
+                unsigned& e = m.table[n];
+                if ((e >> 16) == 0) {
+                    e = (unsigned)li | (1u << 16);
+                } else {
+                    if (n != last) return fail(SPTB_ERR_STATE, "tile build: centre cell not contiguous");
+                    e += 1u << 16;
+                }
+                last = n;
+            }
+    }
+    // irregular samples (after n_reg): fix-up entries per touched cell outside dense tiles
+    std::vector<std::pair<int, int2>> fx;
+    for (int64_t r = sp.n_reg; r < p->N; ++r) {
+        const int smp = order[r];
+        for (int k = rp[smp]; k < rp[smp + 1]; ++k) {
             const int gx = col[k] % X, gy = col[k] / X;
-            cnt[(gy / STILE) * t.ntx + gx / STILE + 1]++;
+            const int qx = std::min(std::max(gx - 1, 0) / STILE, npx - 1), qy = gy / STILE;
+            if (is_dense[(size_t)qy * npx + qx]) continue;
+            const int slot = (gy - cy[smp] + 1) * 3 + (gx - cx[smp] + 1);
+            fx.push_back({col[k], make_int2((int)r, slot)});
         }
     }
-    for (int64_t i = 0; i < ntiles; ++i) cnt[i + 1] += cnt[i];
-    // entry key within a tile: cell (6 bits) | s' (31 bits) | slot (4 bits), in s' order
-    std::vector<uint64_t> ent((size_t)std::max<int64_t>(cnt[ntiles], 1));
-    {
-        std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-        for (int64_t r = 0; r < N; ++r) {
-            const int s = order[r];
-            for (int k = rp[s]; k < rp[s + 1]; ++k) {
-                const int gx = col[k] % X, gy = col[k] / X;
-                const int ti = (gy / STILE) * t.ntx + gx / STILE;
-                const int cell = (gy % STILE) * STILE + gx % STILE;
-                const int slot = (gy - cy[s] + 1) * 3 + (gx - cx[s] + 1);
-                ent[fill[ti]++] = ((uint64_t)cell << 40) | ((uint64_t)r << 4) | (uint64_t)slot;
-            }
+    std::stable_sort(fx.begin(), fx.end(), [](const std::pair<int, int2>& a, const std::pair<int, int2>& b) {
+        return a.first < b.first;
+    });
+    std::vector<int> fcell, fptr(1, 0);
+    std::vector<int2> fent;
+    for (size_t i = 0; i < fx.size(); ++i) {
+        if (i == 0 || fx[i].first != fx[i - 1].first) {
+            if (i) fptr.push_back((int)fent.size());
+            fcell.push_back(fx[i].first);
         }
+        fent.push_back(fx[i].second);
     }
-    std::vector<int> tile_chunk(ntiles + 1, 0), samp;
-    std::vector<int4> chunks;
-    std::vector<unsigned> meta;
-    std::vector<int> smp;
-    std::vector<int> cellcnt(STILE * STILE + 1);
-    for (int64_t ti = 0; ti < ntiles; ++ti) {
-        tile_chunk[ti] = (int)chunks.size();
-        const int64_t a = cnt[ti], b = cnt[ti + 1];
-        if (a == b) continue;
-        smp.clear();
-        for (int64_t i = a; i < b; ++i) smp.push_back((int)((ent[i] >> 4) & 0x7fffffffULL));
-        std::sort(smp.begin(), smp.end());
-        smp.erase(std::unique(smp.begin(), smp.end()), smp.end());
-        // entries sorted by (s', slot) within the tile; stable by cell later
-        std::sort(ent.begin() + a, ent.begin() + b, [](uint64_t u, uint64_t v) {
-            return (u & 0xffffffffffULL) < (v & 0xffffffffffULL);
-        });
-        const int ns = (int)smp.size();
-        int64_t ei = a;
-        for (int s0 = 0; s0 < ns; s0 += STILE_CHUNK) {
-            const int s1 = std::min(ns, s0 + STILE_CHUNK);
-            const int last = smp[s1 - 1];
-            int64_t ej = ei;
-            while (ej < b && (int)((ent[ej] >> 4) & 0x7fffffffULL) <= last) ++ej;
-            std::fill(cellcnt.begin(), cellcnt.end(), 0);
-            for (int64_t i = ei; i < ej; ++i) cellcnt[(int)(ent[i] >> 40) + 1]++;
-            for (int i = 0; i < STILE * STILE; ++i) cellcnt[i + 1] += cellcnt[i];
-            const int nent = (int)(ej - ei);
-            const size_t moff = meta.size();
-            const int mlen = (nent + STILE * STILE + 1 + 3) & ~3;
-            meta.resize(moff + mlen, 0);
-            for (int i = 0; i <= STILE * STILE; ++i) meta[moff + i] = (unsigned)cellcnt[i];
-            std::vector<int> pos(cellcnt.begin(), cellcnt.end() - 1);
-            int li = s0;
-            for (int64_t i = ei; i < ej; ++i) {  // ascending (s', slot): per-cell order preserved
-                const int sp = (int)((ent[i] >> 4) & 0x7fffffffULL);
-                while (smp[li] != sp) ++li;
-                const int cell = (int)(ent[i] >> 40);
-                meta[moff + STILE * STILE + 1 + pos[cell]++] =
-                    ((unsigned)(li - s0) << 16) | (unsigned)((li - s0) * SLOT_STRIDE + (int)(ent[i] & 15));
-            }
-            t.max_meta = std::max(t.max_meta, mlen);
-            chunks.push_back(make_int4((int)ti, (int)samp.size(), s1 - s0, (int)moff));
-            samp.insert(samp.end(), smp.begin() + s0, smp.begin() + s1);
-            ei = ej;
-        }
-    }
-    tile_chunk[ntiles] = (int)chunks.size();
-    if (meta.size() >= (size_t)INT32_MAX) return fail(SPTB_ERR_STATE, "tile metadata too large");
-    t.n_chunks = (int64_t)chunks.size();
-    SPTB_CUDA(cudaMalloc(&t.tile_chunk, sizeof(int) * tile_chunk.size()));
-    SPTB_CUDA(cudaMalloc(&t.chunks, sizeof(int4) * std::max<size_t>(chunks.size(), 1)));
-    SPTB_CUDA(cudaMalloc(&t.samp, sizeof(int) * std::max<size_t>(samp.size(), 1)));
-    SPTB_CUDA(cudaMalloc(&t.meta, sizeof(unsigned) * std::max<size_t>(meta.size(), 4)));
-    SPTB_CUDA(cudaMemcpy(t.tile_chunk, tile_chunk.data(), sizeof(int) * tile_chunk.size(), cudaMemcpyHostToDevice));
-    if (!chunks.empty()) {
-        SPTB_CUDA(cudaMemcpy(t.chunks, chunks.data(), sizeof(int4) * chunks.size(), cudaMemcpyHostToDevice));
-        SPTB_CUDA(cudaMemcpy(t.samp, samp.data(), sizeof(int) * samp.size(), cudaMemcpyHostToDevice));
-        SPTB_CUDA(cudaMemcpy(t.meta, meta.data(), sizeof(unsigned) * meta.size(), cudaMemcpyHostToDevice));
+    if (!fx.empty()) fptr.push_back((int)fent.size());
+    t.n_sparse = (int)sparse.size();
+    t.n_dense = (int)dense.size();
+    t.n_fix = (int)fcell.size();
+    SPTB_CUDA(cudaMalloc(&t.meta, sizeof(STileMeta) * std::max<size_t>(meta.size(), 1)));
+    SPTB_CUDA(cudaMemcpy(t.meta, meta.data(), sizeof(STileMeta) * meta.size(), cudaMemcpyHostToDevice));
+    SPTB_CUDA(cudaMalloc(&t.sparse, sizeof(int) * std::max<size_t>(sparse.size(), 1)));
+    SPTB_CUDA(cudaMalloc(&t.dense, sizeof(int) * std::max<size_t>(dense.size(), 1)));
+    if (!sparse.empty())
+        SPTB_CUDA(cudaMemcpy(t.sparse, sparse.data(), sizeof(int) * sparse.size(), cudaMemcpyHostToDevice));
+    if (!dense.empty())
+        SPTB_CUDA(cudaMemcpy(t.dense, dense.data(), sizeof(int) * dense.size(), cudaMemcpyHostToDevice));
+    if (t.n_fix) {
+        SPTB_CUDA(cudaMalloc(&t.fix_cell, sizeof(int) * fcell.size()));
+        SPTB_CUDA(cudaMalloc(&t.fix_ptr, sizeof(int) * fptr.size()));
+        SPTB_CUDA(cudaMalloc(&t.fix_ent, sizeof(int2) * fent.size()));
+        SPTB_CUDA(cudaMemcpy(t.fix_cell, fcell.data(), sizeof(int) * fcell.size(), cudaMemcpyHostToDevice));
+        SPTB_CUDA(cudaMemcpy(t.fix_ptr, fptr.data(), sizeof(int) * fptr.size(), cudaMemcpyHostToDevice));
+        SPTB_CUDA(cudaMemcpy(t.fix_ent, fent.data(), sizeof(int2) * fent.size(), cudaMemcpyHostToDevice));
     }
     return SPTB_OK;
 }
