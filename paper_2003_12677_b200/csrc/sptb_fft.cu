@@ -1,0 +1,313 @@
+// Fused detector-axis FFT kernels (complex64, n_p = 2^k, 128 <= n_p <= 4096).
+//
+// The reference applies fft_P (ortho) to every projection row before S and
+// ifft_P after S^H (operators.py:162-165, 178-182).  With cuFFT the device path
+// was pack (caller slices -> complex [b][t][p]) + FFT1 + a permuting transpose
+// to the SpMM operand layout [s'][b] -- three passes over the sinogram batch.
+// These kernels do it in one: a CTA owns one angle t and BG batch columns,
+// reads the caller's real slice pairs (or complex slices) straight from the
+// input, runs the FFT in shared memory (Stockham autosort, radix 8 then 4/2,
+// XOR-swizzled buffer: every stage's reads and writes are bank-conflict free)
+// and writes each frequency p as a BG * 8-byte run of row perm[t * n_p + p].
+// The inverse kernel is the mirror: gather rows [s'][b], inverse FFT, scale
+// by 1/n_p and write the caller's real pairs (or complex slices).
+// Twiddles come from a per-plan table computed in double on the host.
+#include "sptb_internal.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace sptb {
+
+namespace {
+
+constexpr int FT = 256;   // threads per CTA
+constexpr int FBG = 4;    // batch columns per CTA (32-byte output runs)
+
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 3) & 15); }
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ float2 mul_mi(float2 a) {
+    return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2(float2* v) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+}
+template <bool INV>
+__device__ __forceinline__ void dft4(float2* v) {  // in natural order, out natural order
+    const float2 d0 = cadd(v[0], v[2]), d1 = csub(v[0], v[2]);
+    const float2 d2 = cadd(v[1], v[3]), d3 = mul_mi<INV>(csub(v[1], v[3]));
+    v[0] = cadd(d0, d2);
+    v[2] = csub(d0, d2);
+    v[1] = cadd(d1, d3);
+    v[3] = csub(d1, d3);
+}
+template <bool INV>
+__device__ __forceinline__ void dft8(float2* v) {
+    constexpr float h = 0.70710678118654752440f;
+    float2 e[4], o[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        e[r] = cadd(v[r], v[r + 4]);
+        o[r] = csub(v[r], v[r + 4]);
+    }
+    // o[r] *= w8^r, w8 = exp(-+ i pi / 4)
+    o[1] = INV ? make_float2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
+               : make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    o[2] = mul_mi<INV>(o[2]);
+    o[3] = INV ? make_float2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
+               : make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+    dft4<INV>(e);
+    dft4<INV>(o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = e[k];
+        v[2 * k + 1] = o[k];
+    }
+}
+
+// One in-place Stockham stage (sub-transform length Ns = 2^LNS, radix 2^LR)
+// of FBG transforms of length N = 2^LOGN held in buf[b * N + swz(i)], then the
+// remaining stages.  tw[k] = exp(-2 pi i k / N).
+template <int LOGN, int LNS, bool INV>
+__device__ __forceinline__ void fft_stage(float2* buf, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, NS = 1 << LNS;
+    constexpr int LR = (LOGN - LNS) >= 3 ? 3 : (LOGN - LNS);
+    constexpr int R = 1 << LR, NBF = N >> LR;
+    constexpr int NB = (NBF * FBG + FT - 1) / FT;  // butterflies per thread
+    float2 v[NB][R];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const int g = threadIdx.x + q * FT;
+        if (g < NBF * FBG) {
+            const int b = g / NBF, j = g - b * NBF;
+            const float2* src = buf + b * N;
+            const int ts = (j & (NS - 1)) * (N / (NS * R));  // twiddle step
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 x = src[swz(j + r * NBF)];
+                if (NS > 1 && r > 0) {
+                    float2 w = __ldg(tw + ((r * ts) & (N - 1)));
+                    if (INV) w.y = -w.y;
+                    x = cmul(x, w);
+                }
+                v[q][r] = x;
+            }
+            if constexpr (LR == 3) dft8<INV>(v[q]);
+            else if constexpr (LR == 2) dft4<INV>(v[q]);
+            else dft2<INV>(v[q]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+        const int g = threadIdx.x + q * FT;
+        if (g < NBF * FBG) {
+            const int b = g / NBF, j = g - b * NBF;
+            float2* dst = buf + b * N;
+            const int k = j & (NS - 1);
+            const int o = (j - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) dst[swz(o + r * NS)] = v[q][r];
+        }
+    }
+    __syncthreads();
+    if constexpr (LNS + LR < LOGN) fft_stage<LOGN, LNS + LR, INV>(buf, tw);
+}
+
+template <int LOGN, bool INV>
+__device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__ tw) {
+    fft_stage<LOGN, 0, INV>(buf, tw);
+}
+
+// caller slices -> FFT along p -> q[perm[t * N + p]][b]
+template <int LOGN>
+__global__ void __launch_bounds__(FT, 3)
+k_fft1_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, int nb, int T,
+           const int* __restrict__ perm, const float2* __restrict__ tw, float2* __restrict__ q, int B) {
+    constexpr int N = 1 << LOGN;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int t = blockIdx.y, b0 = blockIdx.x * FBG;  // batch groups of one angle run back to back
+    const long long plane = (long long)T * N;
+    // all loads of the CTA in flight before the first shared-memory store
+    constexpr int PER = (N + FT - 1) / FT;
+    float2 z[FBG][PER];
+#pragma unroll
+    for (int b = 0; b < FBG; ++b) {
+        const long long u = u0 + b0 + b;
+        const float* pa = nullptr;
+        const float* pb = nullptr;
+        if (b0 + b < nb) {
+            if (cplx) {
+                pa = in + (u * plane + (long long)t * N) * 2;
+            } else {
+                pa = in + (2 * u) * plane + (long long)t * N;
+                pb = (2 * u + 1 < n) ? in + (2 * u + 1) * plane + (long long)t * N : nullptr;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = threadIdx.x + k * FT;
+            z[b][k] = make_float2(0.f, 0.f);
+            if (pa && i < N) {
+                if (cplx) {
+                    z[b][k] = __ldg(reinterpret_cast<const float2*>(pa) + i);
+                } else {
+                    z[b][k].x = __ldg(pa + i);
+                    if (pb) z[b][k].y = __ldg(pb + i);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < FBG; ++b)
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (threadIdx.x + k * FT < N) fbuf[b * N + swz(threadIdx.x + k * FT)] = z[b][k];
+    __syncthreads();
+    fft_smem<LOGN, false>(fbuf, tw);
+    const int* pr = perm + (long long)t * N;
+    for (int i = threadIdx.x; i < N; i += FT) {
+        float2* dst = q + (size_t)__ldg(pr + i) * B + b0;
+        const int si = swz(i);
+        const float4 lo = make_float4(fbuf[si].x, fbuf[si].y, fbuf[N + si].x, fbuf[N + si].y);
+        const float4 hi = make_float4(fbuf[2 * N + si].x, fbuf[2 * N + si].y, fbuf[3 * N + si].x, fbuf[3 * N + si].y);
+        reinterpret_cast<float4*>(dst)[0] = lo;
+        reinterpret_cast<float4*>(dst)[1] = hi;
+    }
+}
+
+// q[perm[t * N + p]][b] -> inverse FFT along p, * scale -> caller slices
+template <int LOGN>
+__global__ void __launch_bounds__(FT, 3)
+k_fft1_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, const float2* __restrict__ tw,
+           float scale, float* __restrict__ out, int cplx, long long n, long long u0, int nb, int T) {
+    constexpr int N = 1 << LOGN;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int t = blockIdx.y, b0 = blockIdx.x * FBG;  // batch groups of one angle run back to back
+    const int* pr = perm + (long long)t * N;
+    for (int i = threadIdx.x; i < N; i += FT) {
+        const float4* src = reinterpret_cast<const float4*>(q + (size_t)__ldg(pr + i) * B + b0);
+        const float4 lo = __ldg(src), hi = __ldg(src + 1);
+        const int si = swz(i);
+        fbuf[si] = make_float2(lo.x, lo.y);
+        fbuf[N + si] = make_float2(lo.z, lo.w);
+        fbuf[2 * N + si] = make_float2(hi.x, hi.y);
+        fbuf[3 * N + si] = make_float2(hi.z, hi.w);
+    }
+    __syncthreads();
+    fft_smem<LOGN, true>(fbuf, tw);
+    const long long plane = (long long)T * N;
+    for (int b = 0; b < FBG; ++b) {
+        if (b0 + b >= nb) break;
+        const long long u = u0 + b0 + b;
+        float* pa;
+        float* pb = nullptr;
+        if (cplx) {
+            pa = out + (u * plane + (long long)t * N) * 2;
+        } else {
+            pa = out + (2 * u) * plane + (long long)t * N;
+            if (2 * u + 1 < n) pb = out + (2 * u + 1) * plane + (long long)t * N;
+        }
+        for (int i = threadIdx.x; i < N; i += FT) {
+            const float2 z = fbuf[b * N + swz(i)];
+            if (cplx) {
+                reinterpret_cast<float2*>(pa)[i] = make_float2(z.x * scale, z.y * scale);
+            } else {
+                pa[i] = z.x * scale;
+                if (pb) pb[i] = z.y * scale;
+            }
+        }
+    }
+}
+
+int fft1_log2(const sptb_plan* p) {
+    const int P = p->P;
+    if (P < 128 || P > 4096 || (P & (P - 1))) return 0;
+    int l = 0;
+    while ((1 << l) < P) ++l;
+    return l;
+}
+
+int ensure_tw(sptb_plan* p) {
+    if (p->tw1) return SPTB_OK;
+    std::vector<float2> h(p->P);
+    for (int k = 0; k < p->P; ++k) {
+        const double a = -2.0 * M_PI * (double)k / (double)p->P;
+        h[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    SPTB_CUDA(cudaMalloc(&p->tw1, sizeof(float2) * p->P));
+    SPTB_CUDA(cudaMemcpy(p->tw1, h.data(), sizeof(float2) * p->P, cudaMemcpyHostToDevice));
+    return SPTB_OK;
+}
+
+template <int LOGN>
+int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
+               cudaStream_t st) {
+    const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
+    SPTB_CUDA(cudaFuncSetAttribute(k_fft1_fwd<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_fft1_fwd<LOGN><<<dim3((unsigned)(B / FBG), (unsigned)p->T), FT, sm, st>>>(
+        (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
+        (const float2*)p->tw1, (float2*)q, B);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+template <int LOGN>
+int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
+               cudaStream_t st) {
+    const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
+    SPTB_CUDA(cudaFuncSetAttribute(k_fft1_inv<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_fft1_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), FT, sm, st>>>(
+        (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
+        (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+}  // namespace
+
+// usable: complex64 plan, f32 caller data, n_p = 2^k in [128, 4096], B a multiple of FBG
+bool fft1_fused_ok(const sptb_plan* p, int fmt, int B) {
+    return p->prec == SPTB_PREC_F32 && !(fmt & SPTB_FMT_F64) && fft1_log2(p) > 0 && B % FBG == 0 &&
+           !getenv("SPTB_NO_FUSED_FFT1");
+}
+
+int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
+                    cudaStream_t st) {
+    SPTB_TRY(ensure_tw(p));
+    switch (fft1_log2(p)) {
+        case 7: return fwd_launch<7>(p, in, fmt, n, u0, nb, B, q, st);
+        case 8: return fwd_launch<8>(p, in, fmt, n, u0, nb, B, q, st);
+        case 9: return fwd_launch<9>(p, in, fmt, n, u0, nb, B, q, st);
+        case 10: return fwd_launch<10>(p, in, fmt, n, u0, nb, B, q, st);
+        case 11: return fwd_launch<11>(p, in, fmt, n, u0, nb, B, q, st);
+        case 12: return fwd_launch<12>(p, in, fmt, n, u0, nb, B, q, st);
+    }
+    return fail(SPTB_ERR_ARG, "fused FFT1: unsupported n_p");
+}
+
+int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
+                    cudaStream_t st) {
+    SPTB_TRY(ensure_tw(p));
+    switch (fft1_log2(p)) {
+        case 7: return inv_launch<7>(p, q, B, out, fmt, n, u0, nb, st);
+        case 8: return inv_launch<8>(p, q, B, out, fmt, n, u0, nb, st);
+        case 9: return inv_launch<9>(p, q, B, out, fmt, n, u0, nb, st);
+        case 10: return inv_launch<10>(p, q, B, out, fmt, n, u0, nb, st);
+        case 11: return inv_launch<11>(p, q, B, out, fmt, n, u0, nb, st);
+        case 12: return inv_launch<12>(p, q, B, out, fmt, n, u0, nb, st);
+    }
+    return fail(SPTB_ERR_ARG, "fused FFT1: unsupported n_p");
+}
+
+}  // namespace sptb

@@ -205,6 +205,7 @@ struct sptb_plan {
     void* pin[NPIPE] = {};
     void* pout[NPIPE] = {};
     size_t pin_bytes[NPIPE] = {}, pout_bytes[NPIPE] = {};
+    void* tw1 = nullptr;       // fused FFT1 twiddles exp(-2 pi i k / n_p), complex64
     // reduction scratch
     double* red = nullptr;
     size_t red_len = 0;
@@ -267,6 +268,12 @@ inline DevCSR s_permuted(const sptb_plan* p) {
     return A;
 }
 
+// fused detector-axis FFTs (sptb_fft.cu): caller slices -> FFT1 -> [s'][b], and back
+bool fft1_fused_ok(const sptb_plan* p, int fmt, int B);
+int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
+                    cudaStream_t st);
+int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
+                    cudaStream_t st);
 // pack caller slices -> complex [b][len] (optionally times a real plane)
 // unpack complex [b][len] -> caller slices, times plane (optional) * scale
 template <typename R>

@@ -225,6 +225,8 @@ int radon_batch(sptb_plan* p, const void* in, int in_fmt, int64_t n, int64_t u0,
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_FORWARD));
     // patch SpMM reads the batch-outer FFT2 output directly -> [s'][b]
     SPTB_TRY(launch_spmm_sh_patch<R>(p, p->G0, p->S1, B, nullptr, st));
+    if (fft1_fused_ok(p, out_fmt, B))  // gather [s'][b] + IFFT1 + unpack in one pass
+        return launch_fft1_inv(p, p->S1, B, out, out_fmt, on, ou0, nb, st);
     SPTB_TRY(launch_transpose_unpermute<R>(p->S1, p->S0, p->shp.order, B, p->N, st));
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_INVERSE));
     return launch_unpack<R>(p->S0, p->N, nullptr, 1.0 / p->P, out, out_fmt, on, ou0, nb, st);
@@ -237,9 +239,13 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     FFTPlans* f;
     SPTB_TRY(get_fft(p, B, &f));
     cudaStream_t st = p->stream;
-    SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
-    SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
-    SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
+    if (fft1_fused_ok(p, in_fmt, B)) {  // pack + FFT1 + permute in one pass
+        SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st));
+    } else {
+        SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
+        SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
+        SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
+    }
     const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
     SPTB_TRY(launch_spmm_s<R>(p, vals, p->S1, p->G0, B, st));
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_INVERSE));
@@ -347,7 +353,7 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
                     p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->stl.sparse,
                     p->stl.dense, p->stl.meta, p->stl.fix_cell, p->stl.fix_ptr, p->stl.fix_ent,
-                    p->stl.swval};
+                    p->stl.swval, p->tw1};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (int k = 0; k < sptb_plan::NPIPE; ++k) {
