@@ -436,6 +436,62 @@ k_unpack(const typename Cplx<R>::T* __restrict__ z, long long len, const R* __re
     }
 }
 
+// f32 real pairs, 4 consecutive elements per thread: 128-bit loads and stores
+// (the scalar kernels above reach ~55% of HBM bandwidth on 2048^2 planes)
+__global__ void __launch_bounds__(256)
+k_unpack4(const float4* __restrict__ z, long long len4, const float4* __restrict__ plane, float scale,
+          float4* __restrict__ out, long long n, long long u0) {
+    const int b = blockIdx.y;
+    const long long u = u0 + b;
+    const float4* src = z + (size_t)b * len4 * 2;
+    float4* pa = out + (size_t)(2 * u) * len4;
+    float4* pb = (2 * u + 1 < n) ? out + (size_t)(2 * u + 1) * len4 : nullptr;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 v0 = __ldcs(src + 2 * i), v1 = __ldcs(src + 2 * i + 1);
+        float4 f = make_float4(scale, scale, scale, scale);
+        if (plane) {
+            const float4 d = __ldg(plane + i);
+            f = make_float4(d.x * scale, d.y * scale, d.z * scale, d.w * scale);
+        }
+        __stcs(pa + i, make_float4(v0.x * f.x, v0.z * f.y, v1.x * f.z, v1.z * f.w));
+        if (pb) __stcs(pb + i, make_float4(v0.y * f.x, v0.w * f.y, v1.y * f.z, v1.w * f.w));
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_pack4(const float4* __restrict__ in, long long len4, const float4* __restrict__ plane, long long n,
+        long long u0, int nb, float4* __restrict__ out) {
+    const int b = blockIdx.y;
+    const long long u = u0 + b;
+    float4* dst = out + (size_t)b * len4 * 2;
+    const float4* pa = b < nb ? in + (size_t)(2 * u) * len4 : nullptr;
+    const float4* pb = (b < nb && 2 * u + 1 < n) ? in + (size_t)(2 * u + 1) * len4 : nullptr;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len4;
+         i += (long long)gridDim.x * blockDim.x) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+        if (pa) a = __ldcs(pa + i);
+        if (pb) c = __ldcs(pb + i);
+        if (plane) {
+            const float4 d = __ldg(plane + i);
+            a = make_float4(a.x * d.x, a.y * d.y, a.z * d.z, a.w * d.w);
+            c = make_float4(c.x * d.x, c.y * d.y, c.z * d.z, c.w * d.w);
+        }
+        dst[2 * i] = make_float4(a.x, c.x, a.y, c.y);
+        dst[2 * i + 1] = make_float4(a.z, c.z, a.w, c.w);
+    }
+}
+
+static bool vec4_ok(const void* a, const void* b, long long len) {
+    return len % 4 == 0 && ((uintptr_t)a % 16) == 0 && ((uintptr_t)b % 16) == 0;
+}
+
+static dim3 vec_grid(long long len4, int nplanes) {
+    const long long per = (len4 + 255) / 256;
+    const long long cap = std::max<long long>(1, 148LL * 32 / std::max(1, nplanes));
+    return dim3((unsigned)std::max<long long>(1, std::min(per, cap)), (unsigned)nplanes);
+}
+
 static int grid_for(long long total) {
     long long g = (total + 255) / 256;
     return (int)std::min<long long>(g, 148LL * 32);
@@ -453,6 +509,14 @@ int launch_pack(const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, i
                 const void* plane, void* out, cudaStream_t st) {
     using C = typename Cplx<R>::T;
     const bool cplx = fmt & SPTB_FMT_COMPLEX;
+    if constexpr (sizeof(R) == 4) {
+        if (!cplx && !(fmt & SPTB_FMT_F64) && vec4_ok(in, out, len) && ((uintptr_t)plane % 16) == 0) {
+            k_pack4<<<vec_grid(len / 4, B), 256, 0, st>>>((const float4*)in, len / 4, (const float4*)plane, n,
+                                                         u0, nb, (float4*)out);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
+    }
     const dim3 grid = plane_grid(len, B);
     if (fmt & SPTB_FMT_F64)
         k_pack<double, R><<<grid, 256, 0, st>>>((const double*)in, cplx, n, u0, nb, len,
@@ -471,6 +535,14 @@ int launch_unpack(const void* in, int64_t len, const void* plane, double scale, 
                   int fmt, int64_t n, int64_t u0, int nb, cudaStream_t st) {
     using C = typename Cplx<R>::T;
     const bool cplx = fmt & SPTB_FMT_COMPLEX;
+    if constexpr (sizeof(R) == 4) {
+        if (!cplx && !(fmt & SPTB_FMT_F64) && vec4_ok(in, out, len) && ((uintptr_t)plane % 16) == 0) {
+            k_unpack4<<<vec_grid(len / 4, nb), 256, 0, st>>>((const float4*)in, len / 4, (const float4*)plane,
+                                                            (float)scale, (float4*)out, n, u0);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
+    }
     const dim3 grid = plane_grid(len, nb);
     if (fmt & SPTB_FMT_F64)
         k_unpack<double, R><<<grid, 256, 0, st>>>((const C*)in, len, (const R*)plane, (R)scale,
