@@ -15,6 +15,7 @@
 #include "sptb_internal.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace sptb {
@@ -231,6 +232,249 @@ k_fft1_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident variant for n_p = 2^LOGN, 512 <= n_p <= 4096: 16 points
+// per thread, n_p / 16 threads per transform, three stages of radix 16, 16
+// and n_p / 256 computed in registers (the radix-16 DFT as 4 x 4 with
+// constant twiddles), two shared-memory exchanges between them.  The XOR
+// swizzle i ^ ((i >> 4) & 15) makes every exchange pattern conflict free.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int swz4(int i) { return i ^ ((i >> 4) & 15); }
+
+template <bool INV>
+__device__ __forceinline__ float2 tw16(int m) {  // W16^m, m in [0, 16)
+    constexpr float c[16] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                             0.f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                             -1.f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                             0.f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+    // sin(2 pi m / 16) = cos(2 pi (m - 4) / 16)
+    const float sn = c[(m + 12) & 15];
+    return make_float2(c[m & 15], INV ? sn : -sn);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft16(float2* v) {
+    float2 a[4][4];  // a[r1][k0]
+#pragma unroll
+    for (int r1 = 0; r1 < 4; ++r1) {
+        float2 t[4] = {v[r1], v[r1 + 4], v[r1 + 8], v[r1 + 12]};
+        dft4<INV>(t);
+#pragma unroll
+        for (int k0 = 0; k0 < 4; ++k0) a[r1][k0] = (r1 * k0) ? cmul(t[k0], tw16<INV>(r1 * k0)) : t[k0];
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < 4; ++k0) {
+        float2 t[4] = {a[0][k0], a[1][k0], a[2][k0], a[3][k0]};
+        dft4<INV>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[k0 + 4 * k1] = t[k1];
+    }
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft_r(float2* v) {
+    if constexpr (R == 16) dft16<INV>(v);
+    else if constexpr (R == 8) dft8<INV>(v);
+    else if constexpr (R == 4) dft4<INV>(v);
+    else dft2<INV>(v);
+}
+
+// w[r] = W_N^(m r) for r < R (w[0] unused): W_N^m and W_N^(2m) from the
+// table, the rest by products -- each power at most 3 multiplications deep
+template <int R, bool INV>
+__device__ __forceinline__ void twiddle_powers(float2* w, const float2* __restrict__ tw, int m) {
+    float2 w1 = __ldg(tw + m);
+    if (INV) w1.y = -w1.y;
+    w[1] = w1;
+    if constexpr (R > 2) {
+        float2 w2 = __ldg(tw + 2 * m);
+        if (INV) w2.y = -w2.y;
+        w[2] = w2;
+        w[3] = cmul(w2, w1);
+    }
+    if constexpr (R > 4) {
+        const float2 w4 = cmul(w[2], w[2]);
+        w[4] = w4;
+        w[5] = cmul(w4, w[1]);
+        w[6] = cmul(w4, w[2]);
+        w[7] = cmul(w4, w[3]);
+    }
+    if constexpr (R > 8) {
+        const float2 w8 = cmul(w[4], w[4]);
+        w[8] = w8;
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = cmul(w8, w[r - 8]);
+    }
+}
+
+// stages 2 and 3 on one transform held in buf (swizzled); the 16 values of
+// stage 1 are in v; on return buf holds the natural-order transform (when
+// STORE_SMEM) or v holds X[j + n/R3 * r ... ] for the caller (two butterflies
+// of R3 when R3 < 16: v[c * R3 + r] = X[(j + c * T) + 256 * r]).
+template <int LOGN, bool INV>
+__device__ __forceinline__ void fft16_stages(float2* v, float2* buf, int j, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, T = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    // stage 1 output y[16 j + r]
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4(16 * j + r)] = v[r];
+    __syncthreads();
+    // stage 2: Ns = 16, radix 16; twiddles w^r, w = W_256^(j % 16), built by
+    // products of one table load (<= 4 roundings deep)
+    {
+        float2 w[16];
+        twiddle_powers<16, INV>(w, tw, (j & 15) * (N / 256));
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const float2 x = buf[swz4(j + T * r)];
+            v[r] = r ? cmul(x, w[r]) : x;
+        }
+    }
+    dft16<INV>(v);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4((j >> 4) * 256 + (j & 15) + 16 * r)] = v[r];
+    __syncthreads();
+    // stage 3: Ns = 256, radix R3, NB3 butterflies per thread (jj = j + c T)
+#pragma unroll
+    for (int c = 0; c < NB3; ++c) {
+        const int jj = j + c * T;
+        float2 w[R3];
+        twiddle_powers<R3, INV>(w, tw, jj & 255);
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const float2 x = buf[swz4(jj + (N / R3) * r)];
+            v[c * R3 + r] = r ? cmul(x, w[r]) : x;
+        }
+        dft_r<R3, INV>(v + c * R3);
+    }
+}
+
+// caller slices -> FFT along p -> q[perm[t * N + p]][b]; FBG transforms per CTA
+template <int LOGN>
+__global__ void __launch_bounds__(FBG * (1 << LOGN) / 16, 2)
+k_fft1r_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, int nb, int T,
+            const int* __restrict__ perm, const float2* __restrict__ tw, float2* __restrict__ q, int B) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int t = blockIdx.y, b0 = blockIdx.x * FBG;
+    const int b = threadIdx.x / TP, j = threadIdx.x % TP;
+    float2* buf = fbuf + b * N;
+    const long long plane = (long long)T * N;
+    const long long u = u0 + b0 + b;
+    float2 v[16];
+    {
+        const float* pa = nullptr;
+        const float* pb = nullptr;
+        if (b0 + b < nb) {
+            if (cplx) {
+                pa = in + (u * plane + (long long)t * N) * 2;
+            } else {
+                pa = in + (2 * u) * plane + (long long)t * N;
+                pb = (2 * u + 1 < n) ? in + (2 * u + 1) * plane + (long long)t * N : nullptr;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int i = j + TP * r;
+            float2 z = make_float2(0.f, 0.f);
+            if (pa) {
+                if (cplx) z = __ldg(reinterpret_cast<const float2*>(pa) + i);
+                else {
+                    z.x = __ldg(pa + i);
+                    if (pb) z.y = __ldg(pb + i);
+                }
+            }
+            v[r] = z;
+        }
+    }
+    dft16<false>(v);
+    fft16_stages<LOGN, false>(v, buf, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NB3; ++c)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) buf[swz4(j + c * TP + 256 * r)] = v[c * R3 + r];
+    __syncthreads();
+    const int* pr = perm + (long long)t * N;
+    constexpr int NI = N / (FBG * TP);  // = 4: all row indices loaded before any store
+    int rowi[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) rowi[k] = __ldg(pr + threadIdx.x + k * FBG * TP);
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int i = threadIdx.x + k * FBG * TP;
+        float2* dst = q + (size_t)rowi[k] * B + b0;
+        const int si = swz4(i);
+        const float4 lo = make_float4(fbuf[si].x, fbuf[si].y, fbuf[N + si].x, fbuf[N + si].y);
+        const float4 hi = make_float4(fbuf[2 * N + si].x, fbuf[2 * N + si].y, fbuf[3 * N + si].x, fbuf[3 * N + si].y);
+        reinterpret_cast<float4*>(dst)[0] = lo;
+        reinterpret_cast<float4*>(dst)[1] = hi;
+    }
+}
+
+// q[perm[t * N + p]][b] -> inverse FFT along p, * scale -> caller slices
+template <int LOGN>
+__global__ void __launch_bounds__(FBG * (1 << LOGN) / 16, 2)
+k_fft1r_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, const float2* __restrict__ tw,
+            float scale, float* __restrict__ out, int cplx, long long n, long long u0, int nb, int T) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int t = blockIdx.y, b0 = blockIdx.x * FBG;
+    const int b = threadIdx.x / TP, j = threadIdx.x % TP;
+    float2* buf = fbuf + b * N;
+    const int* pr = perm + (long long)t * N;
+    constexpr int NI = N / (FBG * TP);  // = 4: all gathers in flight before any shared store
+    float4 glo[NI], ghi[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const float4* src =
+            reinterpret_cast<const float4*>(q + (size_t)__ldg(pr + threadIdx.x + k * FBG * TP) * B + b0);
+        glo[k] = __ldg(src);
+        ghi[k] = __ldg(src + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int i = threadIdx.x + k * FBG * TP;
+        const float4 lo = glo[k], hi = ghi[k];
+        const int si = swz4(i);
+        fbuf[si] = make_float2(lo.x, lo.y);
+        fbuf[N + si] = make_float2(lo.z, lo.w);
+        fbuf[2 * N + si] = make_float2(hi.x, hi.y);
+        fbuf[3 * N + si] = make_float2(hi.z, hi.w);
+    }
+    __syncthreads();
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = buf[swz4(j + TP * r)];
+    dft16<true>(v);
+    __syncthreads();  // stage 1 reads done before fft16_stages overwrites buf
+    fft16_stages<LOGN, true>(v, buf, j, tw);
+    if (b0 + b >= nb) return;
+    const long long plane = (long long)T * N;
+    const long long u = u0 + b0 + b;
+    float* pa;
+    float* pb = nullptr;
+    if (cplx) {
+        pa = out + (u * plane + (long long)t * N) * 2;
+    } else {
+        pa = out + (2 * u) * plane + (long long)t * N;
+        if (2 * u + 1 < n) pb = out + (2 * u + 1) * plane + (long long)t * N;
+    }
+#pragma unroll
+    for (int c = 0; c < NB3; ++c)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const int i = j + c * TP + 256 * r;
+            const float2 z = v[c * R3 + r];
+            if (cplx) {
+                reinterpret_cast<float2*>(pa)[i] = make_float2(z.x * scale, z.y * scale);
+            } else {
+                pa[i] = z.x * scale;
+                if (pb) pb[i] = z.y * scale;
+            }
+        }
+}
+
 int fft1_log2(const sptb_plan* p) {
     const int P = p->P;
     if (P < 128 || P > 4096 || (P & (P - 1))) return 0;
@@ -255,6 +499,17 @@ template <int LOGN>
 int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
                cudaStream_t st) {
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
+    if constexpr (LOGN >= 9) {
+        if (!getenv("SPTB_FFT1_STOCKHAM")) {
+            constexpr int NT = FBG * (1 << LOGN) / 16;
+            SPTB_CUDA(cudaFuncSetAttribute(k_fft1r_fwd<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_fft1r_fwd<LOGN><<<dim3((unsigned)(B / FBG), (unsigned)p->T), NT, sm, st>>>(
+                (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
+                (const float2*)p->tw1, (float2*)q, B);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
+    }
     SPTB_CUDA(cudaFuncSetAttribute(k_fft1_fwd<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_fft1_fwd<LOGN><<<dim3((unsigned)(B / FBG), (unsigned)p->T), FT, sm, st>>>(
         (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
@@ -266,6 +521,17 @@ template <int LOGN>
 int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                cudaStream_t st) {
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
+    if constexpr (LOGN >= 9) {
+        if (!getenv("SPTB_FFT1_STOCKHAM")) {
+            constexpr int NT = FBG * (1 << LOGN) / 16;
+            SPTB_CUDA(cudaFuncSetAttribute(k_fft1r_inv<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_fft1r_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), NT, sm, st>>>(
+                (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
+                (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
+    }
     SPTB_CUDA(cudaFuncSetAttribute(k_fft1_inv<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_fft1_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), FT, sm, st>>>(
         (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
