@@ -25,6 +25,11 @@
 
 namespace sptb {
 
+// Raise a kernel's dynamic shared-memory limit (and prefer the maximum
+// carveout) once per function: cudaFuncSetAttribute is not free, and the hot
+// launch paths call this every time.
+cudaError_t set_smem_once(const void* func, int bytes);
+
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 void count_launch(int n = 1);

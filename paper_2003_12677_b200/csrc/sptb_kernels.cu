@@ -261,7 +261,7 @@ static int spmm_dispatch(const DevCSR& A, const void* val, const void* x, void* 
     size_t sm = (size_t)(CAP + NCH * Cfg::BB) * sizeof(C);
     if (trans) sm += (size_t)Cfg::TILE * (Cfg::BB + 1) * sizeof(C);
     auto run = [&](auto kern) -> int {
-        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
         kern<<<grid, SPMM_THREADS, sm, st>>>(A.row_ptr, A.col, (const C*)val, (const C*)x,
                                              (C*)y, (const C*)sub, rows);
         SPTB_LAUNCHED();

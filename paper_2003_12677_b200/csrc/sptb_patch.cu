@@ -589,8 +589,7 @@ static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const voi
                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return fail(SPTB_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
         auto run = [&](auto kern) -> int {
-            SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
             kern<<<(unsigned)sp.n_items, PT, sm, st>>>(tm, sp.items, sp.item_perm, (const C*)sp.sval, sp.npx,
                                                        (C*)y, (const C*)sub);
             SPTB_LAUNCHED();
@@ -630,8 +629,7 @@ static int sh_slot_dispatch(const sptb_plan* p, const void* x, void* y, const vo
         const int stage = (int)((sm + 127) & ~(size_t)127);
         const size_t smt = one_per_cta ? sm : 2 * (size_t)stage;
         auto run = [&](auto kern) -> int {
-            SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
-            SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            SPTB_CUDA(set_smem_once((const void*)kern, (int)smt));
             int per_sm = 1, nsm = 148;
             SPTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, smt));
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
@@ -677,7 +675,7 @@ static int sh_patch_dispatch(const sptb_plan* p, const void* x, void* y, const v
         static int dev_cached = -1, per_sm = 0;
         static size_t sm_cached = 0;
         if (dev_cached != p->device || sm_cached != sm) {
-            SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
             SPTB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PT, sm));
             dev_cached = p->device;
             sm_cached = sm;

@@ -33,6 +33,16 @@ int is_device_ptr(const void* ptr, bool* dev) {
     return SPTB_OK;
 }
 
+cudaError_t set_smem_once(const void* func, int bytes) {
+    static std::map<const void*, int> done;
+    auto it = done.find(func);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess) done[func] = bytes;
+    return e;
+}
+
 int ensure_stage(void** buf, size_t* have, size_t need) {
     if (*have >= need) return SPTB_OK;
     if (*buf) cudaFree(*buf);
@@ -142,7 +152,7 @@ static int ensure_pipe(sptb_plan* p) {
 
 // Generic driver over batches of `units` (complex vectors).  Device pointers:
 // one pass per max_batch units on the plan stream.  Host pointers: the units
-// are cut into >= 4 chunks and run as a three-stage pipeline -- H2D of chunk
+// are cut into >= 8 chunks and run as a three-stage pipeline -- H2D of chunk
 // i+1 (io_in stream), compute of chunk i (plan stream), D2H of chunk i-1
 // (io_out stream) -- through NPIPE rotating staging buffers, so the PCIe
 // transfers in both directions overlap each other and the kernels.
@@ -158,7 +168,7 @@ static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void*
     is_device_ptr(out, &dout);
     const int64_t units = n_units(in_fmt, n);
     int64_t chunk = p->max_batch;
-    if (!din || !dout) chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, (units + 3) / 4));
+    if (!din || !dout) chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, (units + 7) / 8));
     SPTB_TRY(ensure_work(p, pow2_at_least((int)std::min<int64_t>(chunk, units))));
     if (din && dout) {
         for (int64_t u0 = 0; u0 < units; u0 += chunk) {

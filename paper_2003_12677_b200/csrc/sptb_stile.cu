@@ -290,15 +290,14 @@ int s_tile_dispatch(const sptb_plan* p, const void* csr_vals, const void* slot, 
     if (t.n_sparse > 0) {
         const size_t sm = std::max((size_t)STILE_CAP * (BB + SLOT_STRIDE) * sizeof(C), so);
         auto kern = k_s_tile<R, BB>;
-        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
         kern<<<t.n_sparse, TT, sm, st>>>(t.sparse, t.meta, npx, p->X, p->Y, p->M, (const C*)x,
                                         (const C*)slot, (C*)y);
         SPTB_LAUNCHED();
     }
     if (t.n_dense > 0) {
         auto kern = k_s_dense<R, BB>;
-        SPTB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)so));
+        SPTB_CUDA(set_smem_once((const void*)kern, (int)so));
         kern<<<t.n_dense, TT, so, st>>>(t.dense, npx, p->X, p->Y, p->M, p->S.row_ptr, p->shp.s_colp,
                                        (const C*)csr_vals, (const C*)x, (C*)y);
         SPTB_LAUNCHED();

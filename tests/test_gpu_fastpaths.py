@@ -1,0 +1,113 @@
+"""The production fast paths against the general ones and the CPU oracle.
+
+Each fast path of the hot loop has a general fallback that the parity tests
+(test_gpu_operators.py) also exercise at small batch sizes.  These tests run
+both on the same batched inputs, at sizes where the fast path is the one
+taken (n_p a power of two >= 128, batch a multiple of 4 complex vectors):
+
+* fused pack + FFT1 + permute / gather + IFFT1 + unpack (sptb_fft.cu):
+  Stockham kernel for n_p <= 256, register radix-16 kernel for n_p >= 512;
+* S^H through the TMA-staged slot kernel vs the LDGSTS slot kernel
+  (sptb_patch.cu; SPTB_NO_TMA selects the latter per call);
+* the oracle (reference algorithm restated on the CPU) on a few slices.
+
+Tolerance: north_star's 1e-4 relative L2 per operator application (complex64).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2003_12677_b200 as m
+    return m
+
+
+def _env(name, value):
+    class _E:
+        def __enter__(self):
+            self.old = os.environ.get(name)
+            os.environ[name] = value
+
+        def __exit__(self, *a):
+            if self.old is None:
+                os.environ.pop(name, None)
+            else:
+                os.environ[name] = self.old
+    return _E()
+
+
+def _ops(sb, n, T, kind="ramlak"):
+    return sb.build_operators(sb.ScanGeometry(n_p=n, n_theta=T), filter_kind=kind, max_batch=8)
+
+
+@pytest.mark.parametrize("n,T", [(128, 45), (256, 90), (512, 60), (1024, 40)])
+def test_fused_fft1_matches_cufft_path(sb, n, T):
+    import torch
+    ops = _ops(sb, n, T)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    sino = torch.randn(13, T, n, device="cuda", generator=g)   # odd stack: 7 units, tail unpaired
+    img = torch.randn(13, n, n, device="cuda", generator=g)
+    rec_fast, sin_fast = ops.iradon(sino), ops.radon(img)
+    with _env("SPTB_NO_FUSED_FFT1", "1"):
+        rec_ref, sin_ref = ops.iradon(sino), ops.radon(img)
+    torch.cuda.synchronize()
+    assert rel(rec_fast.cpu().numpy(), rec_ref.cpu().numpy()) < 1e-5
+    assert rel(sin_fast.cpu().numpy(), sin_ref.cpu().numpy()) < 1e-5
+
+
+def test_fused_fft1_stockham_variant(sb):
+    """n_p >= 512 can also run the smem Stockham kernel (SPTB_FFT1_STOCKHAM)."""
+    import torch
+    ops = _ops(sb, 512, 30)
+    sino = torch.randn(8, 30, 512, device="cuda")
+    a = ops.iradon(sino)
+    with _env("SPTB_FFT1_STOCKHAM", "1"):
+        b = ops.iradon(sino)
+    torch.cuda.synchronize()
+    assert rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
+
+
+def test_sh_tma_matches_ldgsts_kernel(sb):
+    import torch
+    ops = _ops(sb, 256, 90, "none")
+    img = torch.randn(16, 256, 256, device="cuda")
+    a = ops.radon(img)
+    with _env("SPTB_NO_TMA", "1"):
+        b = ops.radon(img)
+    torch.cuda.synchronize()
+    assert rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("n,T", [(256, 180), (512, 120)])
+def test_fast_paths_vs_oracle(sb, n, T):
+    import torch
+    from oracle import OGeom, build_oracle_ops, shepp_logan
+    ops = _ops(sb, n, T)
+    oops = build_oracle_ops(OGeom(n_p=n, n_theta=T), kind="ramlak")
+    u = shepp_logan(n, 8)
+    sino = ops.radon(torch.tensor(u, dtype=torch.float32, device="cuda"))
+    rec = ops.iradon(sino)
+    torch.cuda.synchronize()
+    s_np, r_np = sino.cpu().numpy(), rec.cpu().numpy()
+    for i in (0, 3, 7):
+        want_s = oops.radon(u[i])
+        assert rel(s_np[i], want_s) < 1e-4
+        assert rel(r_np[i], oops.iradon(want_s)) < 1e-4
+
+
+def test_host_pipelined_io_matches_device(sb):
+    """Host buffers go through the chunked H2D / compute / D2H pipeline."""
+    import torch
+    ops = _ops(sb, 256, 90)
+    sino = torch.randn(22, 90, 256)
+    dev = ops.iradon(sino.cuda()).cpu()
+    host = ops.iradon(sino.numpy())
+    assert rel(np.asarray(host), dev.numpy()) < 1e-6
