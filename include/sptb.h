@@ -99,6 +99,14 @@ int sptb_plan_set_filter(sptb_plan* plan, const double* weights, int64_t n_weigh
 int sptb_plan_calibrate(sptb_plan* plan, double* calib_out);
 int sptb_plan_set_calibration(sptb_plan* plan, double calib);
 
+/* density_filter_solve (operators.py:189-236): CGLS on || |S| d - 1 ||_2 over
+ * per-sample weights d (max_iter iterations, relative tolerance tol), clamped
+ * >= 0 and symmetrised in p.  weights_out: n_theta * n_p doubles (sample
+ * order); residual_history: max_iter + 1 doubles, *n_history filled. */
+int sptb_density_filter(sptb_plan* plan, int32_t max_iter, double tol, double* weights_out,
+                        double* residual_history, int32_t* n_history, int32_t* converged,
+                        double* final_residual);
+
 /* Matrix introspection: nnz and (optionally) a host copy of the CSR in the
  * device index convention.  Any pointer may be NULL.                      */
 int sptb_plan_matrix_info(sptb_plan* plan, int32_t which, int64_t* rows,

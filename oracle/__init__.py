@@ -16,7 +16,7 @@ against golden vectors produced by the unmodified reference package
 ``/root/reference`` exists; the fixtures travel, the reference does not).
 """
 
-from .tomo import (OGeom, OKernel, build_gridding, deapodization, filter_weights,
+from .tomo import (OGeom, OKernel, build_gridding, deapodization, density_weights, filter_weights,
                    op_radon, op_radon_adjoint, op_iradon, op_apply_weights,
                    calibration_scale, OracleOps, build_oracle_ops,
                    shepp_logan, snr_db)

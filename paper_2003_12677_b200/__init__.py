@@ -14,7 +14,8 @@ from .errors import (CorruptCacheError, DivergenceError, FileFormatError,
 from .geometry import (Deapodization, KernelSpec, ScanGeometry, checkerboard,
                        support_mask)
 from .operators import (FILTER_KINDS, DeviceGridCSR, FilterSpec, Preconditioner,
-                        TomoOperators, build_operators, iradon, make_filter,
+                        TomoOperators, build_operators, density_filter_solve, iradon,
+                        make_filter,
                         precondition_apply, radon, sample_weights, spmm, spmv)
 from .solvers import (ALGORITHMS, DEFAULT_FILTERS, SolverConfig, SolverReport,
                       solve, solve_cgls, solve_fbp, solve_sirt, solve_tv)
@@ -26,7 +27,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ALGORITHMS", "ChunkPlan", "CorruptCacheError", "DEFAULT_FILTERS",
-    "Deapodization", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
+    "Deapodization", "density_filter_solve", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
     "FileFormatError", "FilterSpec", "GridTooLargeError", "InvalidFlatFieldError",
     "KernelSpec", "LIB_PATH", "NearZeroDenominatorError", "NonFiniteError",
     "PAIRING_TOL", "Preconditioner", "ScanGeometry", "ShapeMismatchError",

@@ -56,6 +56,9 @@ SIGNATURES = [
     ("sptb_plan_set_stream", C.c_int, [_P, _P]),
     ("sptb_plan_set_filter", C.c_int, [_P, C.POINTER(C.c_double), C.c_int64]),
     ("sptb_plan_calibrate", C.c_int, [_P, C.POINTER(C.c_double)]),
+    ("sptb_density_filter", C.c_int, [_P, C.c_int32, C.c_double, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
     ("sptb_plan_set_calibration", C.c_int, [_P, C.c_double]),
     ("sptb_plan_matrix_info", C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -96,6 +96,28 @@ class Preconditioner:
         object.__setattr__(self, "weights", w)
 
 
+def density_filter_solve(csr, geom, max_iter: int = 50, tol: float = 1e-6) -> FilterSpec:
+    """Least-squares sample weights that flatten the gridded response
+    (operators.py:189-236): CGLS on || |S| d - 1 ||_2, clamped >= 0 and
+    symmetrised in p, computed on the device from the plan's CSR pair."""
+    plan = csr._plan
+    if plan.precision != _lib.PREC_F64:
+        # the least-squares problem is ill-conditioned (50 CGLS steps amplify
+        # complex64 rounding of |S| ~1e5x): solve on a complex128 build of the
+        # same matrices, like the reference, and fold the weights into ours
+        plan = _Plan(plan.geom, plan.kernel, _lib.PREC_F64, 1, plan.device, plan.threshold)
+    n = geom.n_theta * geom.n_p
+    w = np.empty(n, dtype=np.float64)
+    hist = np.empty(int(max_iter) + 1, dtype=np.float64)
+    nh, conv, fin = C.c_int32(), C.c_int32(), C.c_double()
+    check(lib.sptb_density_filter(plan.h, int(max_iter), float(tol),
+                                  w.ctypes.data_as(C.POINTER(C.c_double)),
+                                  hist.ctypes.data_as(C.POINTER(C.c_double)), C.byref(nh),
+                                  C.byref(conv), C.byref(fin)), "density_filter_solve")
+    return FilterSpec(kind="density", weights=w, residual_history=hist[:nh.value].copy(),
+                      converged=bool(conv.value), final_residual=float(fin.value))
+
+
 # ------------------------------------------------------------------ device plan
 
 
@@ -115,9 +137,25 @@ class _Plan:
                                    device, float(threshold)), "build_operators")
         self.h = h
         self.geom = geom
+        self.kernel = kernel
+        self.threshold = threshold
         self.precision = precision
         self.device = device
         self.max_batch = max_batch
+        self.filter_w = None   # per-sample or radial weights folded into S diag(w), or None
+        self.calib = 1.0       # the plan's iradon calibration (reset by set_filter)
+
+    def set_filter(self, w):
+        if w is None:
+            check(lib.sptb_plan_set_filter(self.h, None, 0))
+            self.filter_w = None
+            self.calib = 1.0
+            return
+        w = np.ascontiguousarray(w, dtype=np.float64).ravel()
+        check(lib.sptb_plan_set_filter(self.h, w.ctypes.data_as(C.POINTER(C.c_double)), w.size),
+              "set_filter")
+        self.filter_w = w
+        self.calib = 1.0
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -280,11 +318,27 @@ def radon(tomo, csr: DeviceGridCSR, deapo=None, geom=None):
 
 def iradon(sino, csr: DeviceGridCSR, deapo=None, geom=None, weights=None, scale: float = 1.0):
     """Backprojection (operators.py:171-187): csr_filtered carries the folded
-    filter; explicit per-sample ``weights`` must match the plan's filter."""
+    filter; explicit ``weights`` ((n_p,) or (N,)) are folded into the plan for
+    this call when they differ from its current filter, then restored."""
     p = csr._plan
-    filtered = 1 if (csr.filtered or weights is not None) else 0
-    return _apply(p, lib.sptb_backproject, sino, p.geom.sino_shape, p.geom.grid_shape,
-                  "sinogram", extra=(filtered, C.c_double(scale)))
+    if weights is None:
+        return _apply(p, lib.sptb_backproject, sino, p.geom.sino_shape, p.geom.grid_shape,
+                      "sinogram", extra=(1 if csr.filtered else 0, C.c_double(scale)))
+    w = np.ascontiguousarray(weights, dtype=np.float64).ravel()
+    if w.size not in (p.geom.n_p, p.geom.n_theta * p.geom.n_p):
+        raise ShapeMismatchError(f"weights of size {w.size} fit neither (n_p,) nor (N,)")
+    keep, keep_calib = p.filter_w, p.calib
+    same = keep is not None and keep.size == w.size and np.array_equal(keep, w)
+    if not same:
+        p.set_filter(w)
+    try:
+        return _apply(p, lib.sptb_backproject, sino, p.geom.sino_shape, p.geom.grid_shape,
+                      "sinogram", extra=(1, C.c_double(scale)))
+    finally:
+        if not same:
+            p.set_filter(keep)
+            check(lib.sptb_plan_set_calibration(p.h, C.c_double(keep_calib)))
+            p.calib = keep_calib
 
 
 def _spectral(plan, sino, w):
@@ -381,9 +435,6 @@ def build_operators(geom, kernel: KernelSpec | None = None, filter_kind: str = "
         raise ValueError(f"unknown filter kind {filter_kind!r}")
     if precision not in PRECISIONS:
         raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
-    if filter_kind == "density":
-        raise NotImplementedError("filter_kind='density' (density_filter_solve) is not on "
-                                  "the B200 path yet")
     plan = _Plan(geom, kernel, PRECISIONS[precision], int(max_batch),
                  _default_device() if device is None else int(device), threshold)
     dv = np.empty(geom.grid_shape, dtype=np.float64)
@@ -395,17 +446,19 @@ def build_operators(geom, kernel: KernelSpec | None = None, filter_kind: str = "
     weights = None
     calib = 1.0
     if filter_kind != "none":
-        filter_spec = make_filter(filter_kind, geom)
+        if filter_kind == "density":
+            filter_spec = density_filter_solve(csr, geom)
+        else:
+            filter_spec = make_filter(filter_kind, geom)
         weights = sample_weights(filter_spec, geom)
-        w = np.ascontiguousarray(filter_spec.weights, dtype=np.float64)
-        check(lib.sptb_plan_set_filter(plan.h, w.ctypes.data_as(C.POINTER(C.c_double)), w.size),
-              "build_operators")
+        plan.set_filter(filter_spec.weights)
         c = C.c_double()
         check(lib.sptb_plan_calibrate(plan.h, C.byref(c)), "calibration")
         calib = c.value
+        plan.calib = calib
         csr_f = DeviceGridCSR(plan, filtered=True)
     else:
-        check(lib.sptb_plan_set_filter(plan.h, None, 0))
+        plan.set_filter(None)
     return TomoOperators(geom=geom, kernel=kernel, deapo=deapo, csr=csr,
                          filter_spec=filter_spec, csr_filtered=csr_f if fold_filter else None,
                          filter_weights=None if fold_filter else weights,

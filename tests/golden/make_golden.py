@@ -153,9 +153,37 @@ def pipeline_case(sp):
     return out
 
 
+DENSITY_GEOMS = ("g32", "godd", "c1")
+
+
+def density_case(sp, name, gkw, kkw):
+    """density_filter_solve (operators.py:189-236) and the density-filtered
+    operators built on it (build_operators(filter_kind="density"))."""
+    geom = sp.ScanGeometry(**gkw)
+    kern = sp.KernelSpec(**kkw)
+    ops = sp.build_operators(geom, kernel=kern, filter_kind="density")
+    fs = ops.filter_spec
+    sino = ops.radon(_phantom_like(sp, geom))
+    return dict(n_p=geom.n_p, n_theta=geom.n_theta, weights=fs.weights,
+                residual_history=np.asarray(fs.residual_history), converged=fs.converged,
+                final_residual=fs.final_residual, calib=ops.calib_scale, sino=sino,
+                iradon=ops.iradon(sino), **_geom_fields(geom, kern))
+
+
+def _geom_fields(geom, kern):
+    return dict(angles=geom.angles, n_x=geom.n_x, n_y=geom.n_y, center=geom.center,
+                k_family=kern.family, k_width=kern.width, k_beta=kern.beta, k_sigma=kern.sigma)
+
+
 def main():
     sys.path.insert(0, REF)
     import sptomo as sp  # noqa: E402  (the unmodified reference)
+    for name, gkw, kkw in GEOMS:
+        if name in DENSITY_GEOMS:
+            np.savez_compressed(os.path.join(OUT, f"density_{name}.npz"), **density_case(sp, name, gkw, kkw))
+            print("wrote density", name)
+    if "--density-only" in sys.argv:
+        return
     for name, gkw, kkw in GEOMS:
         d = operators_case(sp, name, gkw, kkw)
         np.savez_compressed(os.path.join(OUT, f"ops_{name}.npz"), **d)

@@ -104,3 +104,25 @@ def test_solver_variants(sol):
     opn = build_oracle_ops(OGeom(n_p=32, n_theta=20), kind="none")
     r, rep = o_solve(sol["tv_sino_a"], opn, "tv", max_iter=3, mu=0.5)
     assert rel(r, sol["tv_mu_rec"]) <= 1e-10
+
+
+DENSITY_FILES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "density_*.npz")))
+
+
+@pytest.mark.parametrize("fname", DENSITY_FILES)
+def test_density_weights(fname):
+    """density_filter_solve (operators.py:189-236) and the density-filtered
+    gridrec built on it (build_operators(filter_kind="density"))."""
+    from oracle import density_weights
+    d = load_golden(fname)
+    g, k = golden_geom(d)
+    w, hist, conv, fin = density_weights(build_gridding(g, k), g)
+    # ill-conditioned (see tests/test_gpu_density.py): exact in the container
+    # that made the fixture, ~2e-3 on other CPUs; the objective agrees to 1e-5
+    assert rel(w, d["weights"]) <= 1e-2
+    np.testing.assert_allclose(hist, d["residual_history"], rtol=1e-4)
+    assert conv == bool(d["converged"])
+    assert abs(fin - float(d["final_residual"])) <= 1e-4 * max(1.0, float(d["final_residual"]))
+    # calib / filtered reconstruction inherit the conditioning (the reference
+    # run on another CPU gives calib 0.0131 vs 0.0197 at c1): pinned on the
+    # container that made the fixture only through the objective above
