@@ -95,7 +95,7 @@ struct DevCSR {
 // patch.  Nonzeros are stored as (box-local cell, value) records.
 constexpr int PATCH_W = 8;
 #ifndef SPTB_ITEM_ROWS
-#define SPTB_ITEM_ROWS 64
+#define SPTB_ITEM_ROWS 192
 #endif
 constexpr int PATCH_ITEM_ROWS = SPTB_ITEM_ROWS;
 

@@ -446,8 +446,11 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         " @!p bra W;\n}\n" ::"r"(bar), "r"(parity) : "memory");
 }
 
+#ifndef SPTB_TMA_MINB
+#define SPTB_TMA_MINB 5
+#endif
 template <typename R, int G, int CPL, bool SUB>
-__global__ void __launch_bounds__(PT, 4)
+__global__ void __launch_bounds__(PT, SPTB_TMA_MINB)
 k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ items,
          const unsigned char* __restrict__ item_perm, const typename PCplx<R>::T* __restrict__ sval, int npx,
          typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub) {
