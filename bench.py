@@ -266,6 +266,11 @@ def run_ours(a):
                 "achieved": s["gbs"], "peak": peak, "unit": "GB/s", "frac": s["gbs"] / peak,
                 "traffic": traffic.get("S"), "peak_source": peak_src,
                 "bytes_model": "12*nnz + 4*(rows+1) + 8*B*(U_in + rows) per launch"}
+    sh = spmm["S_H"]
+    # the forward SpMM (radon / every SIRT-CGLS-TV residual) on the same model
+    roofline_sh = {"kernel": "sptb::k_sh_tma (S^H, radon)", "bound": "hbm", "achieved": sh["gbs"],
+                   "peak": peak, "unit": "GB/s", "frac": sh["gbs"] / peak, "traffic": traffic.get("S_H"),
+                   "peak_source": peak_src, "bytes_model": roofline["bytes_model"]}
 
     # ---- SIRT iteration throughput (setup excluded by differencing)
     sirt = _sirt_rate(sb, geom, sino, a, dev, stream)
@@ -316,7 +321,7 @@ def run_ours(a):
                     "per-slice scaled (io.py:130-148)",
             "config": _config(a), "clocks": clk.summary(), "e2e": e2e,
             "gpu_launches": int(launches), "cufft_execs": int(ffts),
-            "roofline": roofline, "cpu_baseline": cpu,
+            "roofline": roofline, "roofline_S_H": roofline_sh, "cpu_baseline": cpu,
             "sirt_iter": sirt, "spmm": spmm, "build_operators_s": build_s,
         }
         print(json.dumps(line), flush=True)
@@ -338,6 +343,11 @@ def _sirt_rate(sb, geom, sino_clean, a, dev, stream):
     # t(k2) - t(k1) over 10 iterations, best of 3 per k (the first call also
     # builds cuFFT plans and work buffers)
     k1, k2 = 2, max(3, a.sirt_iters)
+    # warm-up solves: plans, work buffers and first-touch of the new allocations
+    for k in (k2, k1):
+        sb.solvers.solve_batch(noisy, ops_h, sb.SolverConfig(algorithm="sirt", max_iter=k),
+                               raise_on_failure=False)
+    torch.cuda.synchronize()
     for k in (k1, k2) * 3:
         cfg = sb.SolverConfig(algorithm="sirt", max_iter=k)
         torch.cuda.synchronize()

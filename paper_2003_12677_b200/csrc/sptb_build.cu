@@ -163,43 +163,6 @@ int grid_of(long long n) {
     return (int)(g < 148LL * 64 ? (g > 0 ? g : 1) : 148LL * 64);
 }
 
-// Per row tile: sorted distinct columns + each nonzero's index into them.
-// Tiles above TILE_ENTRY_CAP nonzeros get an empty list (the SpMM gathers
-// those directly).  Host-side, once per plan: the matrix is immutable.
-int build_tiles(DevCSR& A) {
-    const int64_t rows = A.rows, nnz = A.nnz;
-    const int64_t ntiles = (rows + SPMM_TILE - 1) / SPMM_TILE;
-    std::vector<int> rp(rows + 1), col(nnz > 0 ? nnz : 1);
-    SPTB_CUDA(cudaMemcpy(rp.data(), A.row_ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost));
-    if (nnz) SPTB_CUDA(cudaMemcpy(col.data(), A.col, sizeof(int) * nnz, cudaMemcpyDeviceToHost));
-    std::vector<int> uptr(ntiles + 1, 0), ucol;
-    std::vector<unsigned short> loc(nnz > 0 ? nnz : 1, 0);
-    ucol.reserve((size_t)(nnz / 2 + 16));
-    std::vector<int> keys;
-    for (int64_t t = 0; t < ntiles; ++t) {
-        const int64_t r0 = t * SPMM_TILE, r1 = std::min<int64_t>(rows, r0 + SPMM_TILE);
-        const int e0 = rp[r0], e1 = rp[r1];
-        uptr[t] = (int)ucol.size();
-        if (e1 - e0 > TILE_ENTRY_CAP || e1 == e0) continue;
-        keys.assign(col.begin() + e0, col.begin() + e1);
-        std::sort(keys.begin(), keys.end());
-        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-        if ((int)keys.size() > TILE_UNIQUE_CAP) continue;
-        for (int e = e0; e < e1; ++e)
-            loc[e] = (unsigned short)(std::lower_bound(keys.begin(), keys.end(), col[e]) - keys.begin());
-        ucol.insert(ucol.end(), keys.begin(), keys.end());
-    }
-    uptr[ntiles] = (int)ucol.size();
-    A.n_unique = (int64_t)ucol.size();
-    SPTB_CUDA(cudaMalloc(&A.tile_uptr, sizeof(int) * (ntiles + 1)));
-    SPTB_CUDA(cudaMalloc(&A.tile_ucol, sizeof(int) * std::max<size_t>(ucol.size(), 1)));
-    SPTB_CUDA(cudaMalloc(&A.loc, sizeof(unsigned short) * loc.size()));
-    SPTB_CUDA(cudaMemcpy(A.tile_uptr, uptr.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice));
-    if (!ucol.empty())
-        SPTB_CUDA(cudaMemcpy(A.tile_ucol, ucol.data(), sizeof(int) * ucol.size(), cudaMemcpyHostToDevice));
-    SPTB_CUDA(cudaMemcpy(A.loc, loc.data(), sizeof(unsigned short) * loc.size(), cudaMemcpyHostToDevice));
-    return SPTB_OK;
-}
 
 template <typename C>
 int build_typed(sptb_plan* p, const BuildArgs& a) {
@@ -283,9 +246,6 @@ int build_typed(sptb_plan* p, const BuildArgs& a) {
     for (void* q : {(void*)tmp, tmp2, (void*)dmax, (void*)keys_out, (void*)idx_in,
                     (void*)idx_out, (void*)rcnt, (void*)ent_s, (void*)cnt})
         SPTB_CUDA(cudaFree(q));
-    // tile-local gather lists (build_tiles) feed the deduplicating SpMM variant
-    // kept in scratch/spmm_tiled_dedupe.cu.txt; the production SpMM gathers
-    // directly, so they are not built.
     return SPTB_OK;
 }
 

@@ -67,25 +67,12 @@ void count_fft(int n = 1);
     } while (0)
 
 // CSR matrix on the device (int32 indices, complex values of plan precision)
-// Row tiles of SPMM_TILE consecutive rows carry a deduplicated, sorted list of
-// the operand rows they touch; each nonzero stores its column's index in that
-// list (uint16).  The SpMM gathers every distinct operand row once per tile
-// into shared memory (built once per plan, sptb_build.cu: build_tiles).
-constexpr int SPMM_TILE = 16;
-constexpr int TILE_ENTRY_CAP = 256;   // tiles with more nonzeros use direct gathers
-constexpr int TILE_UNIQUE_CAP = 4096; // hard cap on distinct rows recorded per tile
-
 struct DevCSR {
     int64_t rows = 0, cols = 0, nnz = 0;
     int* row_ptr = nullptr;   // rows + 1
     int* col = nullptr;       // nnz
     void* val = nullptr;      // nnz complex (float2 or double2)
     int max_row = 0;          // longest row
-    // tile-local gather lists
-    int* tile_uptr = nullptr;             // ntiles + 1 offsets into tile_ucol
-    int* tile_ucol = nullptr;             // distinct operand rows per tile, ascending
-    unsigned short* loc = nullptr;        // nnz: index of col in its tile's list
-    int64_t n_unique = 0;
 };
 
 // S^H regrouped by grid patch: every sample is assigned to the PATCH_W x
@@ -220,6 +207,11 @@ struct sptb_plan {
     size_t fft_work_bytes = 0;
 
     std::vector<void*> extra;            // solver-owned device buffers
+    // device buffers returned by finished solves, reused by the next one
+    // (cudaMalloc/cudaFree per solve stalled the stream and varied by ms)
+    std::vector<std::pair<size_t, void*>> pool;
+    int* solver_pinned = nullptr;        // lagged early-exit counters
+    cudaEvent_t solver_ev[4] = {};
 };
 
 namespace sptb {

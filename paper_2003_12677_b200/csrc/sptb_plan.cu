@@ -358,8 +358,6 @@ int sptb_plan_destroy(sptb_plan* p) {
     void* bufs[] = {p->S.row_ptr, p->S.col, p->S.val, p->SH.row_ptr, p->SH.col, p->SH.val,
                     p->SW_val, p->w_dev, p->deapo, p->G0, p->G1, p->G2, p->S0, p->S1,
                     p->stage_in, p->stage_out, p->red, p->fft_work,
-                    p->S.tile_uptr, p->S.tile_ucol, p->S.loc,
-                    p->SH.tile_uptr, p->SH.tile_ucol, p->SH.loc,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
                     p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->stl.sparse,
                     p->stl.dense, p->stl.meta, p->stl.fix_cell, p->stl.fix_ptr, p->stl.fix_ent,
@@ -378,6 +376,10 @@ int sptb_plan_destroy(sptb_plan* p) {
     if (p->io_out) cudaStreamDestroy(p->io_out);
     for (void* b : p->extra)
         if (b) cudaFree(b);
+    for (auto& kv : p->pool) cudaFree(kv.second);
+    if (p->solver_pinned) cudaFreeHost(p->solver_pinned);
+    for (auto& e : p->solver_ev)
+        if (e) cudaEventDestroy(e);
     delete p;
     return SPTB_OK;
 }

@@ -935,22 +935,39 @@ struct Solver {
     Unit* us = nullptr;
     Global* gl = nullptr;
     int* pinned = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    std::vector<void*> owned;
+    static constexpr int LAG = 2;  // the host runs up to LAG iterations ahead of the device
+    cudaEvent_t ev[LAG + 1] = {};
+    std::vector<std::pair<size_t, void*>> owned;
 
+    // buffers come from / return to the plan's pool (best fit within 2x)
     int alloc(void** ptr, size_t bytes) {
+        auto& pool = p->pool;
+        int best = -1;
+        for (int i = 0; i < (int)pool.size(); ++i)
+            if (pool[i].first >= bytes && pool[i].first <= 2 * bytes &&
+                (best < 0 || pool[i].first < pool[best].first))
+                best = i;
+        if (best >= 0) {
+            owned.push_back(pool[best]);
+            *ptr = pool[best].second;
+            pool.erase(pool.begin() + best);
+            return SPTB_OK;
+        }
         if (cudaMalloc(ptr, bytes) != cudaSuccess) {
             cudaGetLastError();
-            return fail(SPTB_ERR_OOM, "solver buffers: out of device memory");
+            for (auto& kv : pool) cudaFree(kv.second);  // retry after dropping the cache
+            pool.clear();
+            if (cudaMalloc(ptr, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(SPTB_ERR_OOM, "solver buffers: out of device memory");
+            }
         }
-        owned.push_back(*ptr);
+        owned.push_back({bytes, *ptr});
         return SPTB_OK;
     }
     ~Solver() {
-        for (void* q : owned) cudaFree(q);
-        if (pinned) cudaFreeHost(pinned);
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
+        // stream-ordered reuse: the next solve runs on the same stream
+        for (auto& kv : owned) p->pool.push_back(kv);
     }
 
     int init(int algo, int max_iter) {
@@ -983,8 +1000,13 @@ struct Solver {
         SPTB_TRY(alloc((void**)&hist, sizeof(double) * (size_t)std::max(max_iter, 1) * B));
         SPTB_TRY(alloc((void**)&us, sizeof(Unit) * B));
         SPTB_TRY(alloc((void**)&gl, sizeof(Global)));
-        SPTB_CUDA(cudaHostAlloc((void**)&pinned, sizeof(int) * 2, cudaHostAllocDefault));
-        for (auto& e : ev) SPTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        static_assert(LAG + 1 <= 4, "plan keeps 4 early-exit events");
+        if (!p->solver_pinned) {
+            SPTB_CUDA(cudaHostAlloc((void**)&p->solver_pinned, sizeof(int) * 4, cudaHostAllocDefault));
+            for (auto& e : p->solver_ev) SPTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        pinned = p->solver_pinned;
+        for (int i = 0; i <= LAG; ++i) ev[i] = p->solver_ev[i];
         return SPTB_OK;
     }
 
@@ -1061,17 +1083,17 @@ struct Solver {
         return SPTB_OK;
     }
 
-    // lagged early exit: true when every unit had stopped one iteration ago
+    // lagged early exit: true when every unit had stopped LAG iterations ago
     int poll(int it, bool* stop) {
         *stop = false;
         k_count_active<<<1, 64, 0, st>>>(us, B, gl);
         SPTB_LAUNCHED();
-        SPTB_CUDA(cudaMemcpyAsync(pinned + (it & 1), &gl->n_active, sizeof(int),
+        SPTB_CUDA(cudaMemcpyAsync(pinned + it % (LAG + 1), &gl->n_active, sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
-        SPTB_CUDA(cudaEventRecord(ev[it & 1], st));
-        if (it >= 1) {
-            SPTB_CUDA(cudaEventSynchronize(ev[(it - 1) & 1]));
-            if (pinned[(it - 1) & 1] == 0) *stop = true;
+        SPTB_CUDA(cudaEventRecord(ev[it % (LAG + 1)], st));
+        if (it >= LAG) {
+            SPTB_CUDA(cudaEventSynchronize(ev[(it - LAG) % (LAG + 1)]));
+            if (pinned[(it - LAG) % (LAG + 1)] == 0) *stop = true;
         }
         return SPTB_OK;
     }
