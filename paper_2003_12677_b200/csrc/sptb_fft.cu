@@ -522,7 +522,7 @@ int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n
                cudaStream_t st) {
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
     if constexpr (LOGN >= 9) {
-        if (!getenv("SPTB_FFT1_STOCKHAM")) {
+        if (getenv("SPTB_FFT1_R16_INV")) {  // measured: the Stockham inverse is faster (gathered input)
             constexpr int NT = FBG * (1 << LOGN) / 16;
             SPTB_CUDA(set_smem_once((const void*)k_fft1r_inv<LOGN>, (int)sm));
             k_fft1r_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), NT, sm, st>>>(

@@ -64,15 +64,20 @@ def test_fused_fft1_matches_cufft_path(sb, n, T):
 
 
 def test_fused_fft1_stockham_variant(sb):
-    """n_p >= 512 can also run the smem Stockham kernel (SPTB_FFT1_STOCKHAM)."""
+    """n_p >= 512: the forward runs the register radix-16 kernel and the
+    inverse the Stockham kernel by default; both have the other variant."""
     import torch
     ops = _ops(sb, 512, 30)
     sino = torch.randn(8, 30, 512, device="cuda")
-    a = ops.iradon(sino)
+    img = torch.randn(8, 512, 512, device="cuda")
+    a, ra = ops.iradon(sino), ops.radon(img)
     with _env("SPTB_FFT1_STOCKHAM", "1"):
         b = ops.iradon(sino)
+    with _env("SPTB_FFT1_R16_INV", "1"):
+        rb = ops.radon(img)
     torch.cuda.synchronize()
     assert rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
+    assert rel(ra.cpu().numpy(), rb.cpu().numpy()) < 1e-5
 
 
 def test_sh_tma_matches_ldgsts_kernel(sb):
