@@ -61,7 +61,10 @@ __device__ __forceinline__ void cmac(C& acc, const C& a, const C& b) {
 constexpr int SPMM_THREADS = 256;
 constexpr int LMAX = 64;
 constexpr int NCH = 16;
-constexpr int UNR = 8;
+#ifndef SPTB_UNR
+#define SPTB_UNR 8
+#endif
+constexpr int UNR = SPTB_UNR;
 constexpr int CAP = 1024;  // staged nonzeros per tile
 
 template <typename R, int G, int CPL, int CW>
@@ -282,7 +285,10 @@ int launch_spmm<float>(const DevCSR& A, const void* val, const void* x, void* y,
         case 4: return spmm_dispatch<float, 2, 1, 2>(A, val, x, y, trans, sub, st);
         case 8: return spmm_dispatch<float, 4, 1, 2>(A, val, x, y, trans, sub, st);
         case 16: return spmm_dispatch<float, 8, 1, 2>(A, val, x, y, trans, sub, st);
-        case 32: return spmm_dispatch<float, 16, 1, 2>(A, val, x, y, trans, sub, st);
+#ifndef SPTB_S32_G
+#define SPTB_S32_G 16
+#endif
+        case 32: return spmm_dispatch<float, SPTB_S32_G, 16 / SPTB_S32_G, 2>(A, val, x, y, trans, sub, st);
         case 64: return spmm_dispatch<float, 32, 1, 2>(A, val, x, y, trans, sub, st);
     }
     return fail(SPTB_ERR_ARG, "spmm: batch must be a power of two <= 64");

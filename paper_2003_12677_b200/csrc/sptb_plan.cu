@@ -1,6 +1,8 @@
 // Plan lifecycle and the operator entry points of the C ABI (include/sptb.h).
 #include "sptb_internal.cuh"
 
+#include <mutex>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -34,6 +36,8 @@ int is_device_ptr(const void* ptr, bool* dev) {
 }
 
 cudaError_t set_smem_once(const void* func, int bytes) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     static std::map<const void*, int> done;
     auto it = done.find(func);
     if (it != done.end() && it->second >= bytes) return cudaSuccess;
