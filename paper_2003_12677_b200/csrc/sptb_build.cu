@@ -379,7 +379,10 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     }
     sp.n_reg = sp.slot_mode ? cnt[npatch] : N;
     std::vector<int> cls_start;  // slot mode: per patch, s' start of each border class (+ end)
-    if (sp.slot_mode) {
+#ifndef SPTB_CLASS_ORDER
+#define SPTB_CLASS_ORDER 1
+#endif
+    if (sp.slot_mode && SPTB_CLASS_ORDER) {
         // within a patch: border class (TL, T, TR, R, BR, B, BL, L, interior),
         // then stencil-centre cell, then sample.  Every neighbour of the patch
         // then finds the samples it shares with this patch (an edge column/row
@@ -536,7 +539,7 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         SPTB_LAUNCHED();
     }
     SPTB_CUDA(cudaStreamSynchronize(p->stream));
-    if (sp.slot_mode) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order, cnt, cls_start));
+    if (sp.slot_mode && !cls_start.empty()) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order, cnt, cls_start));
     return SPTB_OK;
 }
 

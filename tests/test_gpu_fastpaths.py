@@ -48,7 +48,7 @@ def _ops(sb, n, T, kind="ramlak"):
     return sb.build_operators(sb.ScanGeometry(n_p=n, n_theta=T), filter_kind=kind, max_batch=8)
 
 
-@pytest.mark.parametrize("n,T", [(128, 45), (256, 90), (512, 60), (1024, 40)])
+@pytest.mark.parametrize("n,T", [(128, 45), (256, 90), (512, 60), (1024, 40), (2048, 12), (4096, 6)])
 def test_fused_fft1_matches_cufft_path(sb, n, T):
     import torch
     ops = _ops(sb, n, T)
