@@ -177,9 +177,9 @@ k_fft1_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, in
             if (threadIdx.x + k * FT < N) fbuf[b * N + swz(threadIdx.x + k * FT)] = z[b][k];
     __syncthreads();
     fft_smem<LOGN, false>(fbuf, tw);
-    const int* pr = perm + (long long)t * N;
+    const int* pr = perm ? perm + (long long)t * N : nullptr;
     for (int i = threadIdx.x; i < N; i += FT) {
-        float2* dst = q + (size_t)__ldg(pr + i) * B + b0;
+        float2* dst = q + (size_t)(pr ? __ldg(pr + i) : t * N + i) * B + b0;
         const int si = swz(i);
         const float4 lo = make_float4(fbuf[si].x, fbuf[si].y, fbuf[N + si].x, fbuf[N + si].y);
         const float4 hi = make_float4(fbuf[2 * N + si].x, fbuf[2 * N + si].y, fbuf[3 * N + si].x, fbuf[3 * N + si].y);
@@ -396,11 +396,14 @@ k_fft1r_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, i
 #pragma unroll
         for (int r = 0; r < R3; ++r) buf[swz4(j + c * TP + 256 * r)] = v[c * R3 + r];
     __syncthreads();
-    const int* pr = perm + (long long)t * N;
+    const int* pr = perm ? perm + (long long)t * N : nullptr;
     constexpr int NI = N / (BG * TP);  // = 4: all row indices loaded before any store
     int rowi[NI];
 #pragma unroll
-    for (int k = 0; k < NI; ++k) rowi[k] = __ldg(pr + threadIdx.x + k * BG * TP);
+    for (int k = 0; k < NI; ++k) {
+        const int i = threadIdx.x + k * BG * TP;
+        rowi[k] = perm ? __ldg(pr + i) : t * N + i;  // no perm: sample order (S with original columns)
+    }
 #pragma unroll
     for (int k = 0; k < NI; ++k) {
         const int i = threadIdx.x + k * BG * TP;
@@ -476,6 +479,8 @@ k_fft1r_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, c
         }
 }
 
+const int* g_fwd_perm = nullptr;  // row map of the current forward launch (nullptr: sample order)
+
 int fft1_log2(const sptb_plan* p) {
     const int P = p->P;
     if (P < 128 || P > 4096 || (P & (P - 1))) return 0;
@@ -512,13 +517,13 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
                 const size_t smb = sizeof(float2) * BG * (1 << LOGN);
                 SPTB_CUDA(set_smem_once((const void*)k_fft1r_fwd<LOGN, BG>, (int)smb));
                 k_fft1r_fwd<LOGN, BG><<<dim3((unsigned)(B / BG), (unsigned)p->T), NT, smb, st>>>(
-                    (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
+                    (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, g_fwd_perm,
                     (const float2*)p->tw1, (float2*)q, B);
             } else {
                 constexpr int NT = FBG * (1 << LOGN) / 16;
                 SPTB_CUDA(set_smem_once((const void*)k_fft1r_fwd<LOGN, FBG>, (int)sm));
                 k_fft1r_fwd<LOGN, FBG><<<dim3((unsigned)(B / FBG), (unsigned)p->T), NT, sm, st>>>(
-                    (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
+                    (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, g_fwd_perm,
                     (const float2*)p->tw1, (float2*)q, B);
             }
             SPTB_LAUNCHED();
@@ -527,7 +532,7 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
     }
     SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd<LOGN>, (int)sm));
     k_fft1_fwd<LOGN><<<dim3((unsigned)(B / FBG), (unsigned)p->T), FT, sm, st>>>(
-        (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, p->shp.perm,
+        (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, g_fwd_perm,
         (const float2*)p->tw1, (float2*)q, B);
     SPTB_LAUNCHED();
     return SPTB_OK;
@@ -564,8 +569,9 @@ bool fft1_fused_ok(const sptb_plan* p, int fmt, int B) {
 }
 
 int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool permute) {
     SPTB_TRY(ensure_tw(p));
+    g_fwd_perm = permute ? p->shp.perm : nullptr;
     switch (fft1_log2(p)) {
         case 7: return fwd_launch<7>(p, in, fmt, n, u0, nb, B, q, st);
         case 8: return fwd_launch<8>(p, in, fmt, n, u0, nb, B, q, st);

@@ -267,8 +267,10 @@ inline DevCSR s_permuted(const sptb_plan* p) {
 
 // fused detector-axis FFTs (sptb_fft.cu): caller slices -> FFT1 -> [s'][b], and back
 bool fft1_fused_ok(const sptb_plan* p, int fmt, int B);
+// permute: rows perm[s] (the patch order s') for S with renumbered columns;
+// false: rows in sample order s for S with its original columns
 int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
-                    cudaStream_t st);
+                    cudaStream_t st, bool permute = true);
 int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                     cudaStream_t st);
 // pack caller slices -> complex [b][len] (optionally times a real plane)

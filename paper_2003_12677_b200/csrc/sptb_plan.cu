@@ -1,6 +1,7 @@
 // Plan lifecycle and the operator entry points of the C ABI (include/sptb.h).
 #include "sptb_internal.cuh"
 
+#include <cstdlib>
 #include <mutex>
 
 #include <algorithm>
@@ -253,15 +254,22 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     FFTPlans* f;
     SPTB_TRY(get_fft(p, B, &f));
     cudaStream_t st = p->stream;
-    if (fft1_fused_ok(p, in_fmt, B)) {  // pack + FFT1 + permute in one pass
-        SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st));
-    } else {
-        SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
-        SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
-        SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
-    }
     const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-    SPTB_TRY(launch_spmm_s<R>(p, vals, p->S1, p->G0, B, st));
+    if (fft1_fused_ok(p, in_fmt, B) && !getenv("SPTB_FFT1_PERM")) {
+        // pack + FFT1 in one pass, rows left in sample order: the row gather
+        // of S reads them through its original column indices (no permutation)
+        SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st, false));
+        SPTB_TRY(launch_spmm<R>(p->S, vals, p->S1, p->G0, B, true, nullptr, st));
+    } else {
+        if (fft1_fused_ok(p, in_fmt, B)) {  // pack + FFT1 + permute in one pass
+            SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st));
+        } else {
+            SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
+            SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
+            SPTB_TRY(launch_transpose_permute<R>(p->S0, p->S1, p->shp.perm, B, p->N, st));
+        }
+        SPTB_TRY(launch_spmm_s<R>(p, vals, p->S1, p->G0, B, st));
+    }
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_INVERSE));
     return launch_unpack<R>(p->G0, p->M, p->deapo, scale / p->P, out, out_fmt, on, ou0, nb, st);
 }
