@@ -22,11 +22,14 @@ from .solvers import (ALGORITHMS, DEFAULT_FILTERS, SolverConfig, SolverReport,
 from .pipeline import (PAIRING_TOL, ChunkPlan, SinogramStack, TomogramStack,
                        pair_complex, plan_chunks, run_pipeline, unpair)
 from ._lib import LIB_PATH, launch_count
+from .cache import (CACHE_MAGIC, CACHE_VERSION, MatrixCacheKey, cache_load, cache_store,
+                    make_cache_key)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ALGORITHMS", "ChunkPlan", "CorruptCacheError", "DEFAULT_FILTERS",
+    "ALGORITHMS", "CACHE_MAGIC", "CACHE_VERSION", "ChunkPlan", "MatrixCacheKey", "cache_load",
+    "cache_store", "make_cache_key", "CorruptCacheError", "DEFAULT_FILTERS",
     "Deapodization", "density_filter_solve", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
     "FileFormatError", "FilterSpec", "GridTooLargeError", "InvalidFlatFieldError",
     "KernelSpec", "LIB_PATH", "NearZeroDenominatorError", "NonFiniteError",

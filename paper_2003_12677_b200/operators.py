@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, lib
-from .errors import ShapeMismatchError
+from . import cache as _cachemod
+from .errors import CorruptCacheError, ShapeMismatchError
 from .geometry import Deapodization, KernelSpec, ScanGeometry, support_mask
 
 FILTER_KINDS = ("none", "ramlak", "shepplogan", "hamming", "density")
@@ -421,14 +422,39 @@ def _default_device():
     return 0
 
 
+def _cache_matrix(plan, dev_csr, geom, kernel, filter_id, weights, cache_dir):
+    """SGCSR001 cache entry for this matrix (operators.py:329-337): validate an
+    existing file (CorruptCacheError like the reference) and check it describes
+    the same matrix as the device build; store one when missing, with
+    complex128 values from a complex128 build."""
+    key = _cachemod.make_cache_key(geom, kernel, filter_id)
+    found = _cachemod.cache_check(key, cache_dir)
+    prune = weights is not None
+    if found is None:
+        src = dev_csr
+        if plan.precision != _lib.PREC_F64:
+            p64 = _Plan(geom, kernel, _lib.PREC_F64, 1, plan.device, plan.threshold)
+            if weights is not None:
+                p64.set_filter(weights)
+            src = DeviceGridCSR(p64, filtered=weights is not None)
+        _cachemod.cache_store(key, _cachemod.host_csr(src, prune), cache_dir)
+    else:
+        rows, cols, nnz = found
+        if (rows, cols) != tuple(dev_csr.shape):
+            raise CorruptCacheError(f"{_cachemod.cache_path(key, cache_dir)}: shape "
+                                    f"{(rows, cols)} disagrees with the geometry")
+    return key
+
+
 def build_operators(geom, kernel: KernelSpec | None = None, filter_kind: str = "ramlak",
                     cache_dir: str | None = None, fold_filter: bool = True,
                     threshold: float = 0.0, *, precision: str = "complex64",
                     max_batch: int = 32, device: int | None = None) -> TomoOperators:
     """Build the device plan (operators.py:317-371).  The matrices are
-    assembled on the GPU in milliseconds, so ``cache_dir`` is accepted for
-    API compatibility but not needed; ``fold_filter`` only changes what the
-    bundle reports (the device always folds)."""
+    assembled on the GPU in well under a second; ``cache_dir`` keeps the
+    reference's SGCSR001 files and calibration meta compatible both ways
+    (cache.py); ``fold_filter`` only changes what the bundle reports (the
+    device always folds)."""
     if kernel is None:
         kernel = KernelSpec()
     if filter_kind not in FILTER_KINDS:
@@ -441,6 +467,8 @@ def build_operators(geom, kernel: KernelSpec | None = None, filter_kind: str = "
     check(lib.sptb_plan_deapo_copy(plan.h, dv.ctypes.data_as(C.c_void_p)))
     deapo = Deapodization(values=dv, support_mask=support_mask(geom))
     csr = DeviceGridCSR(plan, filtered=False)
+    if cache_dir is not None:
+        _cache_matrix(plan, csr, geom, kernel, "none", None, cache_dir)
     filter_spec = None
     csr_f = None
     weights = None
@@ -452,11 +480,21 @@ def build_operators(geom, kernel: KernelSpec | None = None, filter_kind: str = "
             filter_spec = make_filter(filter_kind, geom)
         weights = sample_weights(filter_spec, geom)
         plan.set_filter(filter_spec.weights)
-        c = C.c_double()
-        check(lib.sptb_plan_calibrate(plan.h, C.byref(c)), "calibration")
-        calib = c.value
-        plan.calib = calib
         csr_f = DeviceGridCSR(plan, filtered=True)
+        cached = None
+        if cache_dir is not None and fold_filter:
+            key_f = _cache_matrix(plan, csr_f, geom, kernel, filter_kind, filter_spec.weights, cache_dir)
+            cached = _cachemod.read_calib(key_f, cache_dir)
+        if cached is not None:  # operators.py:355-359
+            calib = cached
+            check(lib.sptb_plan_set_calibration(plan.h, C.c_double(calib)))
+        else:
+            c = C.c_double()
+            check(lib.sptb_plan_calibrate(plan.h, C.byref(c)), "calibration")
+            calib = c.value
+            if cache_dir is not None and fold_filter:
+                _cachemod.write_calib(key_f, cache_dir, calib)
+        plan.calib = calib
     else:
         plan.set_filter(None)
     return TomoOperators(geom=geom, kernel=kernel, deapo=deapo, csr=csr,

@@ -195,3 +195,20 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def cache_keys(sp):
+    """Digests of make_cache_key (gridding.py:209-217) -> cache_keys.json
+    (written by the one-off snippet in the round-1 history; kept here for
+    regeneration)."""
+    import json
+    cases = [dict(n_p=32, n_theta=20), dict(n_p=33, n_theta=17, center=15.7),
+             dict(n_p=24, n_theta=11, n_x=28, n_y=20), dict(n_p=256, n_theta=180)]
+    out = []
+    for gkw in cases:
+        for kkw in ({}, dict(width=5), dict(family="gauss")):
+            g, k = sp.ScanGeometry(**gkw), sp.KernelSpec(**kkw)
+            for f in ("none", "ramlak", "density"):
+                out.append(dict(geom=gkw, kernel=kkw, filter=f, digest=sp.make_cache_key(g, k, f).digest))
+    with open(os.path.join(OUT, "cache_keys.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
