@@ -22,14 +22,20 @@ from .solvers import (ALGORITHMS, DEFAULT_FILTERS, SolverConfig, SolverReport,
 from .pipeline import (PAIRING_TOL, ChunkPlan, SinogramStack, TomogramStack,
                        pair_complex, plan_chunks, run_pipeline, unpair)
 from ._lib import LIB_PATH, launch_count
-from .cache import (CACHE_MAGIC, CACHE_VERSION, MatrixCacheKey, cache_load, cache_store,
-                    make_cache_key)
+from .cache import (CACHE_MAGIC, CACHE_VERSION, MatrixCacheKey, SparseGridCSR, build_matrix,
+                    cache_load, cache_store, make_cache_key)
+from .io import (KIND_INTENSITY, KIND_SINOGRAM, KIND_TOMOGRAM, Metrics, VolumeFile,
+                 compute_metrics, normalize, phantom_shepp_logan, read_volume,
+                 simulate_intensity, sinogram_geometry, snr, write_volume)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ALGORITHMS", "CACHE_MAGIC", "CACHE_VERSION", "ChunkPlan", "MatrixCacheKey", "cache_load",
-    "cache_store", "make_cache_key", "CorruptCacheError", "DEFAULT_FILTERS",
+    "cache_store", "make_cache_key", "SparseGridCSR", "build_matrix", "KIND_INTENSITY",
+    "KIND_SINOGRAM", "KIND_TOMOGRAM", "Metrics", "VolumeFile", "compute_metrics", "normalize",
+    "phantom_shepp_logan", "read_volume", "simulate_intensity", "sinogram_geometry", "snr",
+    "write_volume", "CorruptCacheError", "DEFAULT_FILTERS",
     "Deapodization", "density_filter_solve", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
     "FileFormatError", "FilterSpec", "GridTooLargeError", "InvalidFlatFieldError",
     "KernelSpec", "LIB_PATH", "NearZeroDenominatorError", "NonFiniteError",

@@ -187,6 +187,21 @@ def host_csr(dev_csr, prune_zeros: bool) -> HostGridCSR:
                        SH.indptr.astype(np.int64), SH.indices.astype(np.int64), SH.data)
 
 
+SparseGridCSR = HostGridCSR  # the reference's name for the host matrix pair (gridding.py:47-81)
+
+
+def build_matrix(geom, spec, weights=None, threshold: float = 0.0) -> HostGridCSR:
+    """gridding.py:191-195 on the device: S and S^H (optionally S diag(w),
+    zero entries pruned) assembled by a complex128 plan and copied to the host
+    in the reference's index convention."""
+    from . import _lib
+    from .operators import DeviceGridCSR, _Plan, _default_device
+    plan = _Plan(geom, spec, _lib.PREC_F64, 1, _default_device(), threshold)
+    if weights is not None:
+        plan.set_filter(np.asarray(weights, dtype=np.float64))
+    return host_csr(DeviceGridCSR(plan, filtered=weights is not None), prune_zeros=weights is not None)
+
+
 def read_calib(key: MatrixCacheKey, cache_dir: str):
     p = meta_path(key, cache_dir)
     if not os.path.exists(p):
