@@ -12,7 +12,9 @@ from .errors import (CorruptCacheError, DivergenceError, FileFormatError,
                      NearZeroDenominatorError, NonFiniteError,
                      ShapeMismatchError, SptomoError, WorkerFailureError)
 from .geometry import (Deapodization, KernelSpec, ScanGeometry, checkerboard,
-                       support_mask)
+                       deapodization_compute, kernel_eval, kernel_transform, polar_coords,
+                       stencil_offsets, support_mask)
+from .gridding import SparseCOO, build_coo, coo_to_csr, prune
 from .operators import (FILTER_KINDS, DeviceGridCSR, FilterSpec, Preconditioner,
                         TomoOperators, build_operators, density_filter_solve, iradon,
                         make_filter,
@@ -35,7 +37,8 @@ __all__ = [
     "cache_store", "make_cache_key", "SparseGridCSR", "build_matrix", "KIND_INTENSITY",
     "KIND_SINOGRAM", "KIND_TOMOGRAM", "Metrics", "VolumeFile", "compute_metrics", "normalize",
     "phantom_shepp_logan", "read_volume", "simulate_intensity", "sinogram_geometry", "snr",
-    "write_volume", "CorruptCacheError", "DEFAULT_FILTERS",
+    "write_volume", "deapodization_compute", "kernel_eval", "kernel_transform",
+    "polar_coords", "stencil_offsets", "SparseCOO", "build_coo", "coo_to_csr", "prune", "CorruptCacheError", "DEFAULT_FILTERS",
     "Deapodization", "density_filter_solve", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
     "FileFormatError", "FilterSpec", "GridTooLargeError", "InvalidFlatFieldError",
     "KernelSpec", "LIB_PATH", "NearZeroDenominatorError", "NonFiniteError",

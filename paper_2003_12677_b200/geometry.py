@@ -133,3 +133,69 @@ def checkerboard(geom) -> np.ndarray:
     ix = np.arange(geom.n_x)[None, :] - geom.n_x // 2
     iy = np.arange(geom.n_y)[:, None] - geom.n_y // 2
     return 1.0 - 2.0 * ((ix + iy) % 2)
+
+
+# ------------------------------------------------------------------ reference helpers
+# Setup-time math the reference exposes (geometry.py:146-272).  Nothing on the
+# device path calls these: the plan evaluates the kernel, its transform and the
+# deapodization in sptb_build.cu; they are here so callers of the reference
+# API find the same functions.
+
+
+def kernel_eval(spec: KernelSpec, t) -> np.ndarray:
+    """K(t), exact zero for |t| >= width/2, K(0) = 1 (geometry.py:146-161)."""
+    from scipy.special import i0
+    t = np.asarray(t, dtype=np.float64)
+    inside = np.abs(t) < spec.width / 2.0
+    ts = np.where(inside, t, 0.0)
+    if spec.family == "kb":
+        arg = 1.0 - (2.0 * ts / spec.width) ** 2
+        vals = i0(spec.beta * np.sqrt(np.maximum(arg, 0.0))) / i0(spec.beta)
+    else:
+        vals = np.exp(-0.5 * (ts / spec.sigma) ** 2)
+    return np.where(inside, vals, 0.0)
+
+
+def kernel_transform(spec: KernelSpec, nu) -> np.ndarray:
+    """Continuous Fourier transform of the kernel (geometry.py:164-191): KB in
+    closed form (sinh / sin branch), Gaussian by 64-point Gauss-Legendre."""
+    from scipy.special import i0
+    nu = np.asarray(nu, dtype=np.float64)
+    if spec.family == "kb":
+        w = float(spec.width)
+        z2 = spec.beta ** 2 - (np.pi * w * nu) ** 2
+        pos = z2 > 0
+        zp = np.sqrt(np.where(pos, z2, 1.0))
+        zn = np.sqrt(np.where(pos, 1.0, -z2))
+        small = np.abs(zn) < 1e-12
+        sn = np.where(small, 1.0, np.sin(np.where(small, 1.0, zn)) / np.where(small, 1.0, zn))
+        return np.where(pos, np.sinh(zp) / zp, sn) * (w / i0(spec.beta))
+    half = spec.width / 2.0
+    nodes, weights = np.polynomial.legendre.leggauss(64)
+    t = nodes * half
+    k = np.exp(-0.5 * (t / spec.sigma) ** 2) * weights * half
+    return np.cos(2.0 * np.pi * np.multiply.outer(nu, t)) @ k
+
+
+def stencil_offsets(width: int):
+    """(s_x, s_y) over the width^2 stencil, s_x slowest (geometry.py:194-199)."""
+    h = width // 2
+    r = np.arange(-h, h + 1)
+    sx, sy = np.meshgrid(r, r, indexing="ij")
+    return sx.ravel(), sy.ravel()
+
+
+def polar_coords(geom) -> np.ndarray:
+    """(N, 2) Fourier-plane positions p (cos t, sin t) + (n_x/2, n_y/2),
+    theta-major (geometry.py:202-215)."""
+    p = geom.signed_freqs()
+    px = np.multiply.outer(np.cos(geom.angles), p) + geom.n_x / 2.0
+    py = np.multiply.outer(np.sin(geom.angles), p) + geom.n_y / 2.0
+    return np.stack([px.ravel(), py.ravel()], axis=1)
+
+
+def deapodization_compute(geom, spec: KernelSpec) -> Deapodization:
+    """The plan's deapodization (geometry.py:254-272), computed by the device
+    build (NearZeroDenominatorError like the reference)."""
+    from .operators import _deapo_only
+    return _deapo_only(geom, spec)

@@ -422,6 +422,13 @@ def _default_device():
     return 0
 
 
+def _deapo_only(geom, kernel):
+    plan = _Plan(geom, kernel, _lib.PREC_F64, 1, _default_device(), 0.0)
+    dv = np.empty(geom.grid_shape, dtype=np.float64)
+    check(lib.sptb_plan_deapo_copy(plan.h, dv.ctypes.data_as(C.c_void_p)))
+    return Deapodization(values=dv, support_mask=support_mask(geom))
+
+
 def _cache_matrix(plan, dev_csr, geom, kernel, filter_id, weights, cache_dir):
     """SGCSR001 cache entry for this matrix (operators.py:329-337): validate an
     existing file (CorruptCacheError like the reference) and check it describes

@@ -87,3 +87,16 @@ def test_build_operators_cache_is_reference_format(tmp_path):
     open(p, "r+b").write(b"BADMAGIC")
     with pytest.raises(sb.CorruptCacheError):
         sb.build_operators(g, k, filter_kind="none", cache_dir=str(tmp_path))
+
+
+@pytest.mark.gpu
+def test_gridding_host_views_match_reference():
+    import paper_2003_12677_b200 as sb
+    d = load_golden("ops_g32.npz")
+    g = sb.ScanGeometry(n_p=int(d["n_p"]), n_theta=int(d["n_theta"]))
+    k = sb.KernelSpec()
+    m = sb.coo_to_csr(sb.prune(sb.build_coo(g, k)))
+    np.testing.assert_array_equal(m.row_ptr, d["S_row_ptr"])
+    np.testing.assert_array_equal(m.col_idx, d["S_col_idx"])
+    np.testing.assert_allclose(m.vals, d["S_vals"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(sb.deapodization_compute(g, k).values, d["deapo"], rtol=1e-12)

@@ -48,3 +48,23 @@ def test_helpers_match_reference():
     np.testing.assert_allclose(io.normalize(np.abs(sino) + 0.1, 2.0), d["norm"], rtol=1e-15)
     with pytest.raises(Exception):
         io.normalize(sino, 0.0)
+
+
+def test_geometry_helpers_against_oracle():
+    """kernel_eval / kernel_transform / polar_coords restate the same
+    reference lines as the oracle (geometry.py:146-215)."""
+    import oracle.tomo as ot
+    from paper_2003_12677_b200 import geometry as gm
+    for fam in ("kb", "gauss"):
+        k = gm.KernelSpec(family=fam, width=5)
+        ok = ot.OKernel(family=fam, width=5)
+        t = np.linspace(-3, 3, 61)
+        np.testing.assert_allclose(gm.kernel_eval(k, t), ot.kernel_values(ok, t), rtol=1e-14, atol=0)
+        nu = np.linspace(-0.6, 0.6, 25)
+        np.testing.assert_allclose(gm.kernel_transform(k, nu), ot.kernel_ft(ok, nu), rtol=1e-12)
+    g = gm.ScanGeometry(n_p=16, n_theta=5)
+    sx, sy = gm.stencil_offsets(3)
+    assert list(sx) == [-1, -1, -1, 0, 0, 0, 1, 1, 1] and list(sy) == [-1, 0, 1] * 3
+    pc = gm.polar_coords(g)
+    assert pc.shape == (80, 2)
+    np.testing.assert_allclose(pc[:16, 0], g.signed_freqs() + 8.0)
