@@ -51,6 +51,7 @@ def _args():
     ap.add_argument("--sirt-iters", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solvers", action="store_true", help="skip the CGLS / TV rates")
     return ap.parse_args()
 
 
@@ -274,6 +275,7 @@ def run_ours(a):
 
     # ---- SIRT iteration throughput (setup excluded by differencing)
     sirt = _sirt_rate(sb, geom, sino, a, dev, stream)
+    other = {} if a.no_solvers else _other_solvers(sb, geom, sino, a, dev, stream)
 
     # ---- end to end through the C ABI with host buffers (pinned)
     e2e = None
@@ -322,7 +324,7 @@ def run_ours(a):
             "config": _config(a), "clocks": clk.summary(), "e2e": e2e,
             "gpu_launches": int(launches), "cufft_execs": int(ffts),
             "roofline": roofline, "roofline_S_H": roofline_sh, "cpu_baseline": cpu,
-            "sirt_iter": sirt, "spmm": spmm, "build_operators_s": build_s,
+            "sirt_iter": sirt, **other, "spmm": spmm, "build_operators_s": build_s,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -363,6 +365,33 @@ def _sirt_rate(sb, geom, sino_clean, a, dev, stream):
             "ms_per_iteration": per_iter_ms, "setup_ms": times[k1] - per_iter_ms,
             "iterations_run_min": its, "filter": "hamming",
             "workload": f"SIRT-BB {a.slices} slices 2048^2x1536, 2% noise (BASELINE configs[2] shape)"}
+
+
+def _other_solvers(sb, geom, sino_clean, a, dev, stream):
+    """Informational: CGLS (filter none) and TV (split Bregman, 2 inner CGLS
+    steps) iteration rates on the same 64-slice batch and geometry
+    (BASELINE configs[3] / [4] run these solvers at other sizes)."""
+    import torch
+    ops_n = sb.build_operators(geom, filter_kind="none", max_batch=min(64, max(1, a.slices // 2)))
+    ops_n.plan.bind_stream(stream.cuda_stream)
+    out = {}
+    for algo, k1, k2 in (("cgls", 2, 7), ("tv", 1, 3)):
+        times = {}
+        for k in (k2, k1) + (k1, k2) * 2:
+            cfg = sb.SolverConfig(algorithm=algo, max_iter=k)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, reps, _ = sb.solvers.solve_batch(sino_clean, ops_n, cfg, raise_on_failure=False)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times[k] = min(times.get(k, float("inf")), e0.elapsed_time(e1))
+            its = min(r.iterations_run for r in reps)
+        per = (times[k2] - times[k1]) / (k2 - k1)
+        out[f"{algo}_iter"] = {"value": a.slices * 1e3 / per, "unit": "slice-iterations/s",
+                               "ms_per_iteration": per, "iterations_run_min": its,
+                               "workload": f"{algo.upper()} {a.slices} slices 2048^2x1536, clean, filter none"}
+    return out
 
 
 def _traffic_from_profiles():
