@@ -18,6 +18,10 @@
 #include <cstdlib>
 #include <vector>
 
+#ifndef SPTB_FFT_CARVEOUT
+#define SPTB_FFT_CARVEOUT -1
+#endif
+
 namespace sptb {
 
 namespace {
@@ -530,7 +534,7 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
             return SPTB_OK;
         }
     }
-    SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd<LOGN>, (int)sm));
+    SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
     k_fft1_fwd<LOGN><<<dim3((unsigned)(B / FBG), (unsigned)p->T), FT, sm, st>>>(
         (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, g_fwd_perm,
         (const float2*)p->tw1, (float2*)q, B);
@@ -544,7 +548,7 @@ int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n
     if constexpr (LOGN >= 9) {
         if (getenv("SPTB_FFT1_R16_INV")) {  // measured: the Stockham inverse is faster (gathered input)
             constexpr int NT = FBG * (1 << LOGN) / 16;
-            SPTB_CUDA(set_smem_once((const void*)k_fft1r_inv<LOGN>, (int)sm));
+            SPTB_CUDA(set_smem_once((const void*)k_fft1r_inv<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
             k_fft1r_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), NT, sm, st>>>(
                 (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
                 (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T);
@@ -552,7 +556,7 @@ int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n
             return SPTB_OK;
         }
     }
-    SPTB_CUDA(set_smem_once((const void*)k_fft1_inv<LOGN>, (int)sm));
+    SPTB_CUDA(set_smem_once((const void*)k_fft1_inv<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
     k_fft1_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), FT, sm, st>>>(
         (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
         (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T);

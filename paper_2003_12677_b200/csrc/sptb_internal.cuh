@@ -25,10 +25,11 @@
 
 namespace sptb {
 
-// Raise a kernel's dynamic shared-memory limit (and prefer the maximum
-// carveout) once per function: cudaFuncSetAttribute is not free, and the hot
+// Raise a kernel's dynamic shared-memory limit (and set the preferred smem
+// carveout in percent; < 0 leaves the driver's choice, e.g. for gather
+// kernels that live on L1 hits) once per function: cudaFuncSetAttribute is not free, and the hot
 // launch paths call this every time.
-cudaError_t set_smem_once(const void* func, int bytes);
+cudaError_t set_smem_once(const void* func, int bytes, int carveout = 100);
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

@@ -264,7 +264,9 @@ static int spmm_dispatch(const DevCSR& A, const void* val, const void* x, void* 
     size_t sm = (size_t)(CAP + NCH * Cfg::BB) * sizeof(C);
     if (trans) sm += (size_t)Cfg::TILE * (Cfg::BB + 1) * sizeof(C);
     auto run = [&](auto kern) -> int {
-        SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
+        // the row gather lives on L1 hits of gathered rows: leave the carveout to
+        // the driver (forcing 100% smem cost 5%, 0-25% tripled the time)
+        SPTB_CUDA(set_smem_once((const void*)kern, (int)sm, -1));
         kern<<<grid, SPMM_THREADS, sm, st>>>(A.row_ptr, A.col, (const C*)val, (const C*)x,
                                              (C*)y, (const C*)sub, rows);
         SPTB_LAUNCHED();

@@ -36,14 +36,15 @@ int is_device_ptr(const void* ptr, bool* dev) {
     return SPTB_OK;
 }
 
-cudaError_t set_smem_once(const void* func, int bytes) {
+cudaError_t set_smem_once(const void* func, int bytes, int carveout) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
     static std::map<const void*, int> done;
     auto it = done.find(func);
     if (it != done.end() && it->second >= bytes) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess && carveout >= 0)
+        e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     if (e == cudaSuccess) done[func] = bytes;
     return e;
 }
