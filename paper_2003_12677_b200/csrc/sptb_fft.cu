@@ -483,6 +483,197 @@ k_fft1r_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, c
         }
 }
 
+
+// ---------------------------------------------------------------------------
+// 2-D inverse FFT of the gridded batch G [b][y][x] (after S) fused with the
+// deapodization and the unpack to the caller's real slice pairs.  cuFFT's
+// 2-D plan makes two passes (strided y, contiguous x) and the unpack a third;
+// here the y pass runs in place and the x pass writes the caller's slices:
+//   k_fft2_col: a CTA owns CW = 4 adjacent columns of one plane; lane
+//     (c, j) = (tid % CW, tid / CW) loads rows j + TP r of column c, so each
+//     warp load is 8 rows x 32 contiguous bytes; the radix-16 register FFT
+//     exchanges through a per-column buffer of stride N + 4 (the XOR swizzle
+//     keeps 4 consecutive j in an aligned block of 4 slots, the +4 stride
+//     moves the 4 columns onto disjoint blocks: conflict-free); outputs land
+//     in the same (j + TP q) rows, written straight back.
+//   k_fft2_row: RB rows per CTA, inverse FFT along x, times deapo(y, x) *
+//     scale, real part to slice 2u and imaginary part to slice 2u + 1.
+// ---------------------------------------------------------------------------
+#ifndef SPTB_FFT2_CW
+#define SPTB_FFT2_CW 4
+#endif
+constexpr int CW2 = SPTB_FFT2_CW;  // columns per CTA in the y pass
+constexpr int RB2 = 4;             // rows per CTA in the x pass
+
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1024 / (CW2 * (1 << LOGN) / 16))
+k_fft2_col(float2* __restrict__ g, int X, long long M, int strips, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, LD = N + 16 / CW2;
+    extern __shared__ __align__(16) float2 fbuf[];
+    // column base recomputed after the FFT (keeps it out of the register budget)
+    auto colp = [&]() {
+        const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+        const int b = blockIdx.x / strips, x0 = (blockIdx.x - b * strips) * CW2;
+        return g + (size_t)b * M + (size_t)j * X + x0 + c;
+    };
+    const int step = TP * X;  // rows j + TP r, r = 0..15 (< 2^24 elements)
+    float2 v[16];
+    {
+        const float2* pp = colp();
+#pragma unroll
+        for (int r = 0; r < 16; ++r, pp += step) v[r] = *pp;
+    }
+    dft16<INV>(v);
+    fft16_stages<LOGN, INV>(v, fbuf + (threadIdx.x % CW2) * LD, threadIdx.x / CW2, tw);
+    // output j + TP q + 256 r = j + TP (q + NB3 r) sits in v[q R3 + r]; the
+    // base goes through an opaque move so the compiler recomputes the 16 row
+    // addresses instead of keeping the load addresses live (it spilled them)
+    float2* pp = colp();
+    asm volatile("mov.b64 %0, %0;" : "+l"(pp));
+#pragma unroll
+    for (int m = 0; m < 16; ++m, pp += step) *pp = v[(m % NB3) * R3 + m / NB3];
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
+k_fft2_row_unpack(const float2* __restrict__ g, long long M, int Y, const float* __restrict__ plane, float scale,
+                  float* __restrict__ out, long long n, long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const long long gr = (long long)blockIdx.x * RB2 + rb;  // b * Y + y
+    const int b = (int)(gr / Y), y = (int)(gr - (long long)b * Y);
+    const float2* row = g + (size_t)b * M + (size_t)y * N;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = __ldcs(row + j + TP * r);
+    dft16<true>(v);
+    fft16_stages<LOGN, true>(v, fbuf + rb * N, j, tw);
+    if (b >= nb) return;
+    const long long u = u0 + b;
+    float* pa = out + (size_t)(2 * u) * M + (size_t)y * N;
+    float* pb = (2 * u + 1 < n) ? out + (size_t)(2 * u + 1) * M + (size_t)y * N : nullptr;
+    const float* pl = plane ? plane + (size_t)y * N : nullptr;
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const int x = j + TP * q + 256 * r;
+            const float f = pl ? __ldg(pl + x) * scale : scale;
+            const float2 z = v[q * R3 + r];
+            __stcs(pa + x, z.x * f);
+            if (pb) __stcs(pb + x, z.y * f);
+        }
+}
+
+// radon side: caller real pairs (slices 2u, 2u + 1) times deapo(y, x) ->
+// forward FFT along x -> G row (planes b >= nb are zero-filled: the S^H
+// kernel reads all B planes)
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
+k_fft2_row_pack(const float* __restrict__ in, long long M, int Y, const float* __restrict__ plane, long long n,
+                long long u0, int nb, float2* __restrict__ g, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(16) float2 fbuf[];
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const long long gr = (long long)blockIdx.x * RB2 + rb;  // b * Y + y
+    const int b = (int)(gr / Y), y = (int)(gr - (long long)b * Y);
+    const long long u = u0 + b;
+    const float* pa = b < nb ? in + (size_t)(2 * u) * M + (size_t)y * N : nullptr;
+    const float* pb = (b < nb && 2 * u + 1 < n) ? in + (size_t)(2 * u + 1) * M + (size_t)y * N : nullptr;
+    const float* pl = plane ? plane + (size_t)y * N : nullptr;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int x = j + TP * r;
+        const float d = pl ? __ldg(pl + x) : 1.f;
+        v[r] = make_float2(pa ? __ldcs(pa + x) * d : 0.f, pb ? __ldcs(pb + x) * d : 0.f);
+    }
+    dft16<false>(v);
+    fft16_stages<LOGN, false>(v, fbuf + rb * N, j, tw);
+    float2* row = g + (size_t)b * M + (size_t)y * N;
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) row[j + TP * q + 256 * r] = v[q * R3 + r];
+}
+
+int log2_fft(long long n) {
+    if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
+    int l = 0;
+    while ((1LL << l) < n) ++l;
+    return l;
+}
+
+const float2* twiddles(sptb_plan* p, int logn) {
+    if (!p->twn[logn]) {
+        const int n = 1 << logn;
+        std::vector<float2> h(n);
+        for (int k = 0; k < n; ++k) {
+            const double a = -2.0 * M_PI * (double)k / (double)n;
+            h[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        if (cudaMalloc(&p->twn[logn], sizeof(float2) * n) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(p->twn[logn], h.data(), sizeof(float2) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+            return nullptr;
+    }
+    return (const float2*)p->twn[logn];
+}
+
+template <int LOGN>
+int col_launch(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
+    const int strips = p->X / CW2;
+    k_fft2_col<LOGN, true><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+template <int LOGN>
+int col_launch_fwd(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
+    const int strips = p->X / CW2;
+    k_fft2_col<LOGN, false><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+template <int LOGN>
+int row_pack_launch(sptb_plan* p, const float* in, const float* plane, int64_t n, int64_t u0, int nb, int B,
+                    float2* g, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = RB2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * RB2 * (1 << LOGN));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack<LOGN>, sm, SPTB_FFT_CARVEOUT));
+    k_fft2_row_pack<LOGN><<<(unsigned)(((long long)B * p->Y + RB2 - 1) / RB2), NT, sm, st>>>(
+        in, p->M, p->Y, plane, n, u0, nb, g, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+template <int LOGN>
+int row_launch(sptb_plan* p, const float2* g, const float* plane, float scale, float* out, int64_t n, int64_t u0,
+               int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = RB2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * RB2 * (1 << LOGN));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack<LOGN>, sm, SPTB_FFT_CARVEOUT));
+    k_fft2_row_unpack<LOGN><<<(unsigned)(((long long)nb * p->Y + RB2 - 1) / RB2), NT, sm, st>>>(
+        g, p->M, p->Y, plane, scale, out, n, u0, nb, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
 const int* g_fwd_perm = nullptr;  // row map of the current forward launch (nullptr: sample order)
 
 int fft1_log2(const sptb_plan* p) {
@@ -599,6 +790,58 @@ int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int6
         case 12: return inv_launch<12>(p, q, B, out, fmt, n, u0, nb, st);
     }
     return fail(SPTB_ERR_ARG, "fused FFT1: unsupported n_p");
+}
+
+// usable: complex64 plan, real f32 caller slices, X and Y powers of two in
+// [512, 4096] (the row kernel owns whole rows: Y * nb a multiple of RB2)
+bool fft2_fused_ok(const sptb_plan* p, int fmt) {
+    return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->X) > 0 &&
+           log2_fft(p->Y) > 0 && !getenv("SPTB_NO_FUSED_FFT2");
+}
+
+int launch_fft2_inv_unpack(sptb_plan* p, void* g, const void* plane, double scale, void* out, int64_t n,
+                           int64_t u0, int nb, cudaStream_t st) {
+    float2* G = (float2*)g;
+    int rc;
+    switch (log2_fft(p->Y)) {
+        case 9: rc = col_launch<9>(p, G, nb, st); break;
+        case 10: rc = col_launch<10>(p, G, nb, st); break;
+        case 11: rc = col_launch<11>(p, G, nb, st); break;
+        case 12: rc = col_launch<12>(p, G, nb, st); break;
+        default: return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_y");
+    }
+    if (rc != SPTB_OK) return rc;
+    const float* pl = (const float*)plane;
+    const float sc = (float)scale;
+    switch (log2_fft(p->X)) {
+        case 9: return row_launch<9>(p, G, pl, sc, (float*)out, n, u0, nb, st);
+        case 10: return row_launch<10>(p, G, pl, sc, (float*)out, n, u0, nb, st);
+        case 11: return row_launch<11>(p, G, pl, sc, (float*)out, n, u0, nb, st);
+        case 12: return row_launch<12>(p, G, pl, sc, (float*)out, n, u0, nb, st);
+    }
+    return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_x");
+}
+
+int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_t n, int64_t u0, int nb, int B,
+                         void* g, cudaStream_t st) {
+    float2* G = (float2*)g;
+    const float* pl = (const float*)plane;
+    int rc;
+    switch (log2_fft(p->X)) {
+        case 9: rc = row_pack_launch<9>(p, (const float*)in, pl, n, u0, nb, B, G, st); break;
+        case 10: rc = row_pack_launch<10>(p, (const float*)in, pl, n, u0, nb, B, G, st); break;
+        case 11: rc = row_pack_launch<11>(p, (const float*)in, pl, n, u0, nb, B, G, st); break;
+        case 12: rc = row_pack_launch<12>(p, (const float*)in, pl, n, u0, nb, B, G, st); break;
+        default: return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_x");
+    }
+    if (rc != SPTB_OK) return rc;
+    switch (log2_fft(p->Y)) {  // zero planes stay zero: only the nb filled planes need the y pass
+        case 9: return col_launch_fwd<9>(p, G, nb, st);
+        case 10: return col_launch_fwd<10>(p, G, nb, st);
+        case 11: return col_launch_fwd<11>(p, G, nb, st);
+        case 12: return col_launch_fwd<12>(p, G, nb, st);
+    }
+    return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_y");
 }
 
 }  // namespace sptb

@@ -199,6 +199,7 @@ struct sptb_plan {
     void* pout[NPIPE] = {};
     size_t pin_bytes[NPIPE] = {}, pout_bytes[NPIPE] = {};
     void* tw1 = nullptr;       // fused FFT1 twiddles exp(-2 pi i k / n_p), complex64
+    void* twn[13] = {};        // fused FFT2 twiddles exp(-2 pi i k / 2^L), indexed by L
     // reduction scratch
     double* red = nullptr;
     size_t red_len = 0;
@@ -274,6 +275,14 @@ int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0
                     cudaStream_t st, bool permute = true);
 int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                     cudaStream_t st);
+// 2-D inverse FFT of G [b][y][x] (in place along y) fused with the
+// deapodization and unpack to caller real slice pairs (sptb_fft.cu)
+bool fft2_fused_ok(const sptb_plan* p, int fmt);
+int launch_fft2_inv_unpack(sptb_plan* p, void* g, const void* plane, double scale, void* out, int64_t n,
+                           int64_t u0, int nb, cudaStream_t st);
+// caller real pairs times plane -> forward 2-D FFT -> G [b][y][x], B planes
+int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_t n, int64_t u0, int nb, int B,
+                         void* g, cudaStream_t st);
 // pack caller slices -> complex [b][len] (optionally times a real plane)
 // unpack complex [b][len] -> caller slices, times plane (optional) * scale
 template <typename R>

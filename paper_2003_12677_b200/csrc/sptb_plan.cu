@@ -237,8 +237,12 @@ int radon_batch(sptb_plan* p, const void* in, int in_fmt, int64_t n, int64_t u0,
     FFTPlans* f;
     SPTB_TRY(get_fft(p, B, &f));
     cudaStream_t st = p->stream;
-    SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->M, p->deapo, p->G0, st));
-    SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_FORWARD));
+    if (fft2_fused_ok(p, in_fmt)) {
+        SPTB_TRY(launch_fft2_pack_fwd(p, in, p->deapo, n, u0, nb, B, p->G0, st));
+    } else {
+        SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->M, p->deapo, p->G0, st));
+        SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_FORWARD));
+    }
     // patch SpMM reads the batch-outer FFT2 output directly -> [s'][b]
     SPTB_TRY(launch_spmm_sh_patch<R>(p, p->G0, p->S1, B, nullptr, st));
     if (fft1_fused_ok(p, out_fmt, B))  // gather [s'][b] + IFFT1 + unpack in one pass
@@ -271,6 +275,8 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
         }
         SPTB_TRY(launch_spmm_s<R>(p, vals, p->S1, p->G0, B, st));
     }
+    if (fft2_fused_ok(p, out_fmt))
+        return launch_fft2_inv_unpack(p, p->G0, p->deapo, scale / p->P, out, on, ou0, nb, st);
     SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_INVERSE));
     return launch_unpack<R>(p->G0, p->M, p->deapo, scale / p->P, out, out_fmt, on, ou0, nb, st);
 }
@@ -376,6 +382,8 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->stl.dense, p->stl.meta, p->stl.fix_cell, p->stl.fix_ptr, p->stl.fix_ent,
                     p->stl.swval, p->tw1};
     for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (void* b : p->twn)
         if (b) cudaFree(b);
     for (int k = 0; k < sptb_plan::NPIPE; ++k) {
         if (p->pin[k]) cudaFree(p->pin[k]);

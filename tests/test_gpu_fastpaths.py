@@ -7,6 +7,8 @@ taken (n_p a power of two >= 128, batch a multiple of 4 complex vectors):
 
 * fused pack + FFT1 + permute / gather + IFFT1 + unpack (sptb_fft.cu):
   Stockham kernel for n_p <= 256, register radix-16 kernel for n_p >= 512;
+* fused inverse FFT2 (y pass in place, x pass + deapodization + unpack) vs
+  cuFFT's 2-D plan + unpack (SPTB_NO_FUSED_FFT2);
 * S^H through the TMA-staged slot kernel vs the LDGSTS slot kernel
   (sptb_patch.cu; SPTB_NO_TMA selects the latter per call);
 * the oracle (reference algorithm restated on the CPU) on a few slices.
@@ -61,6 +63,27 @@ def test_fused_fft1_matches_cufft_path(sb, n, T):
     torch.cuda.synchronize()
     assert rel(rec_fast.cpu().numpy(), rec_ref.cpu().numpy()) < 1e-5
     assert rel(sin_fast.cpu().numpy(), sin_ref.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("n,T,nx,ny", [(512, 60, None, None), (1024, 40, None, None), (2048, 12, None, None),
+                                       (4096, 6, None, None), (512, 45, 1024, 512), (1024, 30, 512, 2048)])
+def test_fused_fft2_unpack_matches_cufft_path(sb, n, T, nx, ny):
+    """iradon's y pass + x pass/deapodization/unpack and radon's pack/x pass +
+    y pass vs cuFFT + pack/unpack (square and rectangular grids, odd stack:
+    the last pair has no partner)."""
+    import torch
+    ops = sb.build_operators(sb.ScanGeometry(n_p=n, n_theta=T, n_x=nx, n_y=ny), filter_kind="ramlak",
+                             max_batch=8)
+    g = torch.Generator(device="cuda").manual_seed(n + T)
+    sino = torch.randn(13, T, n, device="cuda", generator=g)
+    img = torch.randn(13, ops.geom.n_y, ops.geom.n_x, device="cuda", generator=g)
+    fast, fast_s = ops.iradon(sino), ops.radon(img)
+    with _env("SPTB_NO_FUSED_FFT2", "1"):
+        ref, ref_s = ops.iradon(sino), ops.radon(img)
+    torch.cuda.synchronize()
+    assert fast.shape == ref.shape
+    assert rel(fast.cpu().numpy(), ref.cpu().numpy()) < 1e-5
+    assert rel(fast_s.cpu().numpy(), ref_s.cpu().numpy()) < 1e-5
 
 
 def test_fused_fft1_stockham_variant(sb):
