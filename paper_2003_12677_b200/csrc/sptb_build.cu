@@ -638,6 +638,12 @@ int build_deapo(sptb_plan* p, const sptb_kernel* k) {
     if (bad)
         return fail(SPTB_ERR_NEAR_ZERO, "kernel transform vanishes at " + std::to_string(bad) +
                                             " supported grid points; narrow the kernel");
+    // separable form for the fused FFT2 kernels: deapo = [dx^2 + dy^2 < r^2] * fx[x] * fy[y]
+    std::vector<float> fxy((size_t)X + Y);
+    for (int x = 0; x < X; ++x) fxy[x] = (float)((((x - X / 2) % 2) == 0 ? 1.0 : -1.0) / ax[x]);
+    for (int y = 0; y < Y; ++y) fxy[(size_t)X + y] = (float)((((y - Y / 2) % 2) == 0 ? 1.0 : -1.0) / ay[y]);
+    SPTB_CUDA(cudaMalloc(&p->deapo_xy, fxy.size() * sizeof(float)));
+    SPTB_CUDA(cudaMemcpy(p->deapo_xy, fxy.data(), fxy.size() * sizeof(float), cudaMemcpyHostToDevice));
     const size_t n = (size_t)X * Y;
     if (p->prec == SPTB_PREC_F64) {
         SPTB_CUDA(cudaMalloc(&p->deapo, n * sizeof(double)));

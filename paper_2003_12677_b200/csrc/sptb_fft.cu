@@ -14,6 +14,9 @@
 // Twiddles come from a per-plan table computed in double on the host.
 #include "sptb_internal.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -23,6 +26,8 @@
 #endif
 
 namespace sptb {
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder();  // sptb_patch.cu
 
 namespace {
 
@@ -566,6 +571,85 @@ k_fft2_row_unpack(const float2* __restrict__ g, long long M, int Y, const float*
         }
 }
 
+// y pass with the strip staged by TMA: N / 256 boxes of 256 rows x CW2
+// columns land in [row][c] order on one mbarrier (no per-lane loads: the LSU
+// queue throttled the LDG version), L2 promotion 256 B so the neighbouring
+// strips' sectors come from the same DRAM bursts
+__device__ __forceinline__ void fbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "FW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra FW;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+#ifndef SPTB_FFT2_TSTORE
+#define SPTB_FFT2_TSTORE 1
+#endif
+template <int LOGN, bool INV, bool TSTORE = SPTB_FFT2_TSTORE>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1024 / (CW2 * (1 << LOGN) / 16))
+k_fft2_col_tma(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ g, int X, long long M, int strips,
+               const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3;
+    // own name: an extern array shares the alignment of its first declaration
+    // (16 for fbuf) and the TMA destination needs 128
+    extern __shared__ __align__(128) unsigned char colbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(colbuf_raw);
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        const int b = blockIdx.x / strips, x0 = (blockIdx.x - b * strips) * CW2;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"((unsigned)(N * CW2 * sizeof(float2))) : "memory");
+#pragma unroll 1
+        for (int k = 0; k < N / 256; ++k)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(fbuf + k * 256 * CW2)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(x0), "r"(256 * k), "r"(b), "r"(sb)
+                : "memory");
+    }
+    __syncthreads();
+    fbar_wait(sb, 0);
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
+    __syncthreads();  // staged strip consumed before the exchange buffers overwrite it
+    dft16<INV>(v);
+    fft16_stages<LOGN, INV>(v, fbuf + c * LD, j, tw);
+    if constexpr (TSTORE) {
+        // the strip leaves the way it came: [row][c] in shared memory, N / 256 TMA stores
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int b = blockIdx.x / strips, x0 = (blockIdx.x - b * strips) * CW2;
+#pragma unroll 1
+            for (int k = 0; k < N / 256; ++k)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                        reinterpret_cast<unsigned long long>(&tmap)),
+                    "r"(x0), "r"(256 * k), "r"(b), "r"((unsigned)__cvta_generic_to_shared(fbuf + k * 256 * CW2))
+                    : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        }
+    } else {
+        float2* pp;
+        {
+            const int b = blockIdx.x / strips, x0 = (blockIdx.x - b * strips) * CW2;
+            pp = g + (size_t)b * M + (size_t)j * X + x0 + c;
+        }
+        const int step = TP * X;
+#pragma unroll
+        for (int m = 0; m < 16; ++m, pp += step) *pp = v[(m % NB3) * R3 + m / NB3];
+    }
+}
+
 // radon side: caller real pairs (slices 2u, 2u + 1) times deapo(y, x) ->
 // forward FFT along x -> G row (planes b >= nb are zero-filled: the S^H
 // kernel reads all B planes)
@@ -598,6 +682,156 @@ k_fft2_row_pack(const float* __restrict__ in, long long M, int Y, const float* _
         for (int r = 0; r < R3; ++r) row[j + TP * q + 256 * r] = v[q * R3 + r];
 }
 
+// Bulk-copy versions of the two row kernels: the RB2 rows of a CTA are
+// contiguous (Y % RB2 == 0), so the input, the deapodization rows and the
+// output each move as one cp.async.bulk per CTA (no per-lane global loads or
+// scalar stores; the LDG/STG versions were LSU-bound).
+// deapodization weight of row y from the separable factors (build_deapo):
+// [dx^2 + dy^2 < r^2] * fx[x] * fy[y] * scale, r = min(X, Y) / 2; dxy == nullptr: scale
+struct Deapo {
+    const float* fx;
+    float fy, s;
+    int dy2, r2, hx;
+    // fx_s: shared copy of the X factors (nullptr when dxy is)
+    __device__ __forceinline__ Deapo(const float* dxy, const float* fx_s, int X, int Y, int y, float scale)
+        : fx(dxy ? fx_s : nullptr), s(scale) {
+        hx = X / 2;
+        const int dy = y - Y / 2, r = min(X, Y) / 2;
+        dy2 = dy * dy;
+        r2 = r * r;
+        fy = dxy ? __ldg(dxy + X + y) * scale : scale;
+    }
+    __device__ __forceinline__ float operator()(int x) const {
+        if (!fx) return s;
+        const int dx = x - hx;
+        return dx * dx + dy2 < r2 ? fx[x] * fy : 0.f;
+    }
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                 "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
+                 : "memory");
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
+k_fft2_row_unpack_b(const float2* __restrict__ g, long long M, int Y, const float* __restrict__ dxy, float scale,
+                    float* __restrict__ out, long long n, long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(128) unsigned char rowbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(rowbuf_raw);  // [RB2][N]
+    float* fxs = reinterpret_cast<float*>(fbuf + RB2 * N);  // [N] x factors of the deapodization
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    const long long gr0 = (long long)blockIdx.x * RB2;
+    const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"(RB2 * N * 8u + (dxy ? N * 4u : 0u))
+                     : "memory");
+        bulk_g2s(fbuf, g + (size_t)b * M + (size_t)y0 * N, RB2 * N * 8u, sb);
+        if (dxy) bulk_g2s(fxs, dxy, N * 4u, sb);
+    }
+    __syncthreads();
+    fbar_wait(sb, 0);
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = fbuf[rb * N + j + TP * r];
+    __syncthreads();
+    dft16<true>(v);
+    fft16_stages<LOGN, true>(v, fbuf + rb * N, j, tw);
+    if (b >= nb) return;  // uniform over the CTA
+    __syncthreads();
+    float* sa = reinterpret_cast<float*>(fbuf);  // [RB2][N] real parts, then [RB2][N] imaginary parts
+    float* sbm = sa + RB2 * N;
+    const Deapo dp(dxy, fxs, N, Y, y0 + rb, scale);
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const int x = j + TP * q + 256 * r;
+            const float f = dp(x);
+            const float2 z = v[q * R3 + r];
+            sa[rb * N + x] = z.x * f;
+            sbm[rb * N + x] = z.y * f;
+        }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const long long u = u0 + b;
+        bulk_s2g(out + (size_t)(2 * u) * M + (size_t)y0 * N, sa, RB2 * N * 4u);
+        if (2 * u + 1 < n) bulk_s2g(out + (size_t)(2 * u + 1) * M + (size_t)y0 * N, sbm, RB2 * N * 4u);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
+k_fft2_row_pack_b(const float* __restrict__ in, long long M, int Y, const float* __restrict__ dxy, long long n,
+                  long long u0, int nb, float2* __restrict__ g, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(128) unsigned char rowbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(rowbuf_raw);
+    float* sa = reinterpret_cast<float*>(fbuf);   // [RB2][N] slice 2u rows
+    float* sbm = sa + RB2 * N;                    // [RB2][N] slice 2u + 1 rows
+    float* fxs = reinterpret_cast<float*>(fbuf + RB2 * N);  // [N] x factors of the deapodization
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    const long long gr0 = (long long)blockIdx.x * RB2;
+    const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+    const long long u = u0 + b;
+    const bool ha = b < nb, hb = b < nb && 2 * u + 1 < n;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        const unsigned bytes = (ha ? RB2 * N * 4u : 0u) + (hb ? RB2 * N * 4u : 0u) + (ha && dxy ? N * 4u : 0u);
+        if (bytes) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(bytes) : "memory");
+            if (ha) bulk_g2s(sa, in + (size_t)(2 * u) * M + (size_t)y0 * N, RB2 * N * 4u, sb);
+            if (hb) bulk_g2s(sbm, in + (size_t)(2 * u + 1) * M + (size_t)y0 * N, RB2 * N * 4u, sb);
+            if (ha && dxy) bulk_g2s(fxs, dxy, N * 4u, sb);
+        }
+    }
+    __syncthreads();
+    if (ha) fbar_wait(sb, 0);
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    float2 v[16];
+    const Deapo dp(dxy, fxs, N, Y, y0 + rb, 1.f);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int x = j + TP * r;
+        const float d = dp(x);
+        v[r] = make_float2(ha ? sa[rb * N + x] * d : 0.f, hb ? sbm[rb * N + x] * d : 0.f);
+    }
+    __syncthreads();
+    dft16<false>(v);
+    fft16_stages<LOGN, false>(v, fbuf + rb * N, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) fbuf[rb * N + j + TP * q + 256 * r] = v[q * R3 + r];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bulk_s2g(g + (size_t)b * M + (size_t)y0 * N, fbuf, RB2 * N * 8u);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+}
+
 int log2_fft(long long n) {
     if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
     int l = 0;
@@ -620,14 +854,39 @@ const float2* twiddles(sptb_plan* p, int logn) {
     return (const float2*)p->twn[logn];
 }
 
+bool col_tma_ok(const void* g) {
+    return tmap_encoder() != nullptr && ((uintptr_t)g % 16) == 0 && !getenv("SPTB_NO_TMA");
+}
+
+// G [b][y][x] complex64 as a 3-D tensor of 8-byte elements; box CW2 x 256 x 1
+int col_tmap(const sptb_plan* p, const void* g, int planes, CUtensorMap* tm) {
+    const cuuint64_t dims[3] = {(cuuint64_t)p->X, (cuuint64_t)p->Y, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)p->X * 8, (cuuint64_t)p->M * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)CW2, 256u, 1u};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult cr = tmap_encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(g), dims, strides,
+                                       box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SPTB_ERR_CUDA, "cuTensorMapEncodeTiled (fft2) failed: " + std::to_string((int)cr));
+    return SPTB_OK;
+}
+
 template <int LOGN>
 int col_launch(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     const float2* tw = twiddles(p, LOGN);
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
-    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
     const int strips = p->X / CW2;
+    if (col_tma_ok(g)) {
+        CUtensorMap tm;
+        SPTB_TRY(col_tmap(p, g, nb, &tm));
+        SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
+        k_fft2_col_tma<LOGN, true><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_col<LOGN, true><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
     SPTB_LAUNCHED();
     return SPTB_OK;
@@ -639,11 +898,26 @@ int col_launch_fwd(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
-    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
     const int strips = p->X / CW2;
+    if (col_tma_ok(g)) {
+        CUtensorMap tm;
+        SPTB_TRY(col_tmap(p, g, nb, &tm));
+        SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
+        k_fft2_col_tma<LOGN, false><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_col<LOGN, false><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
     SPTB_LAUNCHED();
     return SPTB_OK;
+}
+
+// bulk copies: 16-byte aligned caller slices and G (rows are 4 N or 8 N bytes);
+// the deapodization plane is applied from its separable factors (plan->deapo_xy)
+bool row_bulk_ok(const void* a, const void* g) {
+    return ((uintptr_t)a % 16) == 0 && ((uintptr_t)g % 16) == 0 &&
+           !getenv("SPTB_FFT2_NO_BULK");
 }
 
 template <int LOGN>
@@ -652,6 +926,14 @@ int row_pack_launch(sptb_plan* p, const float* in, const float* plane, int64_t n
     const float2* tw = twiddles(p, LOGN);
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = RB2 * (1 << LOGN) / 16;
+    if (row_bulk_ok(in, g)) {
+        const int smb = (int)((8 * RB2 + 4) * (1 << LOGN));
+        SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack_b<LOGN>, smb, SPTB_FFT_CARVEOUT));
+        k_fft2_row_pack_b<LOGN><<<(unsigned)((long long)B * p->Y / RB2), NT, smb, st>>>(
+            in, p->M, p->Y, plane ? p->deapo_xy : nullptr, n, u0, nb, g, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
     const int sm = (int)(sizeof(float2) * RB2 * (1 << LOGN));
     SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack<LOGN>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_row_pack<LOGN><<<(unsigned)(((long long)B * p->Y + RB2 - 1) / RB2), NT, sm, st>>>(
@@ -666,6 +948,14 @@ int row_launch(sptb_plan* p, const float2* g, const float* plane, float scale, f
     const float2* tw = twiddles(p, LOGN);
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = RB2 * (1 << LOGN) / 16;
+    if (row_bulk_ok(out, g)) {
+        const int smb = (int)((8 * RB2 + 4) * (1 << LOGN));
+        SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack_b<LOGN>, smb, SPTB_FFT_CARVEOUT));
+        k_fft2_row_unpack_b<LOGN><<<(unsigned)((long long)nb * p->Y / RB2), NT, smb, st>>>(
+            g, p->M, p->Y, plane ? p->deapo_xy : nullptr, scale, out, n, u0, nb, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
     const int sm = (int)(sizeof(float2) * RB2 * (1 << LOGN));
     SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack<LOGN>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_row_unpack<LOGN><<<(unsigned)(((long long)nb * p->Y + RB2 - 1) / RB2), NT, sm, st>>>(

@@ -177,6 +177,7 @@ struct sptb_plan {
     double calib = 1.0;
 
     void* deapo = nullptr;     // M real (plan precision), row-major [y][x]
+    float* deapo_xy = nullptr; // separable factors: (-1)^(x-X/2)/kx(x) [X], then (-1)^(y-Y/2)/ky(y) [Y]
     std::vector<double> deapo_host;
 
     // work buffers (max_batch complex vectors each)

@@ -553,7 +553,7 @@ k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ item
     }
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {  // shared with sptb_fft.cu
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q;

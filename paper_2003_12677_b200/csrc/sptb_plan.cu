@@ -375,7 +375,7 @@ int sptb_plan_destroy(sptb_plan* p) {
         if (kv.second.fft1) cufftDestroy(kv.second.fft1);
     }
     void* bufs[] = {p->S.row_ptr, p->S.col, p->S.val, p->SH.row_ptr, p->SH.col, p->SH.val,
-                    p->SW_val, p->w_dev, p->deapo, p->G0, p->G1, p->G2, p->S0, p->S1,
+                    p->SW_val, p->w_dev, p->deapo, p->deapo_xy, p->G0, p->G1, p->G2, p->S0, p->S1,
                     p->stage_in, p->stage_out, p->red, p->fft_work,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
                     p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->stl.sparse,
