@@ -360,7 +360,28 @@ __device__ __forceinline__ void fft16_stages(float2* v, float2* buf, int j, cons
 
 // caller slices -> FFT along p -> q[perm[t * N + p]][b]; BG transforms per CTA
 // (BG batch columns: each frequency leaves as one 8 BG-byte run)
-template <int LOGN, int BG>
+// mbarrier wait and 1-D bulk copies (cp.async.bulk) shared by the kernels below
+__device__ __forceinline__ void fbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "FW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra FW;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                 "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
+                 : "memory");
+}
+
+template <int LOGN, int BG, bool BULK = false>
 __global__ void __launch_bounds__(BG * (1 << LOGN) / 16, 1024 / (BG * (1 << LOGN) / 16))
 k_fft1r_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, int nb, int T,
             const int* __restrict__ perm, const float2* __restrict__ tw, float2* __restrict__ q, int B) {
@@ -372,7 +393,37 @@ k_fft1r_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, i
     const long long plane = (long long)T * N;
     const long long u = u0 + b0 + b;
     float2 v[16];
-    {
+    if constexpr (BULK) {
+        // real pairs: the CTA's 2 BG rows (slices 2u, 2u + 1 at angle t) land in
+        // the exchange buffer by bulk copies (the per-lane scalar loads were
+        // LSU-throttled); slice 2(b0 + b) + h row at fbuf floats [(2 b + h) N]
+        float* raw = reinterpret_cast<float*>(fbuf);
+        __shared__ __align__(8) unsigned long long bar;
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            unsigned bytes = 0;
+            for (int k = 0; k < 2 * BG; ++k) {
+                const long long sl = 2 * (u0 + b0) + k;
+                if (b0 + k / 2 < nb && sl < n) bytes += N * 4u;
+            }
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(bytes) : "memory");
+            for (int k = 0; k < 2 * BG; ++k) {
+                const long long sl = 2 * (u0 + b0) + k;
+                if (b0 + k / 2 < nb && sl < n) bulk_g2s(raw + k * N, in + sl * plane + (long long)t * N, N * 4u, sb);
+            }
+        }
+        __syncthreads();
+        fbar_wait(sb, 0);
+        const bool ha = b0 + b < nb, hb = ha && 2 * u + 1 < n;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int i = j + TP * r;
+            v[r] = make_float2(ha ? raw[2 * b * N + i] : 0.f, hb ? raw[(2 * b + 1) * N + i] : 0.f);
+        }
+        __syncthreads();  // staged rows consumed before the exchange overwrites them
+    } else {
         const float* pa = nullptr;
         const float* pb = nullptr;
         if (b0 + b < nb) {
@@ -575,12 +626,6 @@ k_fft2_row_unpack(const float2* __restrict__ g, long long M, int Y, const float*
 // columns land in [row][c] order on one mbarrier (no per-lane loads: the LSU
 // queue throttled the LDG version), L2 promotion 256 B so the neighbouring
 // strips' sectors come from the same DRAM bursts
-__device__ __forceinline__ void fbar_wait(unsigned bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "FW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra FW;\n}\n" ::"r"(bar), "r"(parity) : "memory");
-}
 
 #ifndef SPTB_FFT2_TSTORE
 #define SPTB_FFT2_TSTORE 1
@@ -708,18 +753,6 @@ struct Deapo {
     }
 };
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            (unsigned)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
-                 "r"((unsigned)__cvta_generic_to_shared(src)), "r"(bytes)
-                 : "memory");
-}
 
 template <int LOGN>
 __global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
@@ -1000,6 +1033,13 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
             if (B % BG == 0) {
                 constexpr int NT = BG * (1 << LOGN) / 16;
                 const size_t smb = sizeof(float2) * BG * (1 << LOGN);
+                if (!(fmt & SPTB_FMT_COMPLEX) && ((uintptr_t)in % 16) == 0 && !getenv("SPTB_FFT1_NO_BULK")) {
+                    SPTB_CUDA(set_smem_once((const void*)k_fft1r_fwd<LOGN, BG, true>, (int)smb));
+                    k_fft1r_fwd<LOGN, BG, true><<<dim3((unsigned)(B / BG), (unsigned)p->T), NT, smb, st>>>(
+                        (const float*)in, 0, n, u0, nb, p->T, g_fwd_perm, (const float2*)p->tw1, (float2*)q, B);
+                    SPTB_LAUNCHED();
+                    return SPTB_OK;
+                }
                 SPTB_CUDA(set_smem_once((const void*)k_fft1r_fwd<LOGN, BG>, (int)smb));
                 k_fft1r_fwd<LOGN, BG><<<dim3((unsigned)(B / BG), (unsigned)p->T), NT, smb, st>>>(
                     (const float*)in, (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T, g_fwd_perm,
