@@ -865,6 +865,46 @@ k_fft2_row_pack_b(const float* __restrict__ in, long long M, int Y, const float*
     }
 }
 
+// in-place x pass (solver grids): RB2 contiguous rows in, FFT, back out
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1024 / (RB2 * (1 << LOGN) / 16))
+k_fft2_row_b(float2* __restrict__ g, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    extern __shared__ __align__(128) unsigned char rowbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(rowbuf_raw);
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    float2* rows = g + (size_t)blockIdx.x * RB2 * N;  // planes are whole rows: row index b * Y + y
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(RB2 * N * 8u)
+                     : "memory");
+        bulk_g2s(fbuf, rows, RB2 * N * 8u, sb);
+    }
+    __syncthreads();
+    fbar_wait(sb, 0);
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = fbuf[rb * N + j + TP * r];
+    __syncthreads();
+    dft16<INV>(v);
+    fft16_stages<LOGN, INV>(v, fbuf + rb * N, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) fbuf[rb * N + j + TP * q + 256 * r] = v[q * R3 + r];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bulk_s2g(rows, fbuf, RB2 * N * 8u);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+}
+
 int log2_fft(long long n) {
     if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
     int l = 0;
@@ -951,6 +991,51 @@ int col_launch_fwd(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
 bool row_bulk_ok(const void* a, const void* g) {
     return ((uintptr_t)a % 16) == 0 && ((uintptr_t)g % 16) == 0 &&
            !getenv("SPTB_FFT2_NO_BULK");
+}
+
+template <int LOGN, bool INV>
+int col_launch_dir(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    const int strips = p->X / CW2;
+    CUtensorMap tm;
+    SPTB_TRY(col_tmap(p, g, nb, &tm));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, INV>, sm, SPTB_FFT_CARVEOUT));
+    k_fft2_col_tma<LOGN, INV><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+template <int LOGN, bool INV>
+int row_launch_dir(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+    constexpr int NT = RB2 * (1 << LOGN) / 16;
+    const int sm = (int)(8 * RB2 * (1 << LOGN));
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_row_b<LOGN, INV>, sm, SPTB_FFT_CARVEOUT));
+    k_fft2_row_b<LOGN, INV><<<(unsigned)((long long)nb * p->Y / RB2), NT, sm, st>>>(g, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+template <bool INV>
+int fft2_inplace(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
+    switch (log2_fft(p->Y)) {
+        case 9: SPTB_TRY((col_launch_dir<9, INV>(p, g, nb, st))); break;
+        case 10: SPTB_TRY((col_launch_dir<10, INV>(p, g, nb, st))); break;
+        case 11: SPTB_TRY((col_launch_dir<11, INV>(p, g, nb, st))); break;
+        case 12: SPTB_TRY((col_launch_dir<12, INV>(p, g, nb, st))); break;
+        default: return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_y");
+    }
+    switch (log2_fft(p->X)) {
+        case 9: return row_launch_dir<9, INV>(p, g, nb, st);
+        case 10: return row_launch_dir<10, INV>(p, g, nb, st);
+        case 11: return row_launch_dir<11, INV>(p, g, nb, st);
+        case 12: return row_launch_dir<12, INV>(p, g, nb, st);
+    }
+    return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_x");
 }
 
 template <int LOGN>
@@ -1172,6 +1257,16 @@ int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_
         case 12: return col_launch_fwd<12>(p, G, nb, st);
     }
     return fail(SPTB_ERR_ARG, "fused FFT2: unsupported n_y");
+}
+
+// in-place unnormalised 2-D FFT of nb planes [b][y][x] (cuFFT's sign convention)
+bool fft2_inplace_ok(const sptb_plan* p, const void* g) {
+    return p->prec == SPTB_PREC_F32 && log2_fft(p->X) > 0 && log2_fft(p->Y) > 0 && col_tma_ok(g) &&
+           !getenv("SPTB_NO_FUSED_FFT2");
+}
+
+int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st) {
+    return inverse ? fft2_inplace<true>(p, (float2*)g, nb, st) : fft2_inplace<false>(p, (float2*)g, nb, st);
 }
 
 }  // namespace sptb

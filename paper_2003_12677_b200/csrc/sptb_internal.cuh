@@ -281,6 +281,9 @@ int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int6
 bool fft2_fused_ok(const sptb_plan* p, int fmt);
 int launch_fft2_inv_unpack(sptb_plan* p, void* g, const void* plane, double scale, void* out, int64_t n,
                            int64_t u0, int nb, cudaStream_t st);
+// in-place unnormalised 2-D FFT of nb planes (solver grids), complex64 only
+bool fft2_inplace_ok(const sptb_plan* p, const void* g);
+int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st);
 // caller real pairs times plane -> forward 2-D FFT -> G [b][y][x], B planes
 int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_t n, int64_t u0, int nb, int B,
                          void* g, cudaStream_t st);

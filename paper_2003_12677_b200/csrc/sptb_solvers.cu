@@ -1043,6 +1043,8 @@ struct Solver {
     }
 
     int fft(cufftHandle h, void* z, int dir) {
+        if (z == (void*)W && fft2_inplace_ok(p, z))  // the grid FFT2: fused column + row passes
+            return launch_fft2_inplace(p, z, B, dir == CUFFT_INVERSE, st);
         count_fft();
         if (sizeof(R) == 8)
             SPTB_CUFFT(cufftExecZ2Z(h, (cufftDoubleComplex*)z, (cufftDoubleComplex*)z, dir));

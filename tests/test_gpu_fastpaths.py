@@ -142,3 +142,20 @@ def test_host_pipelined_io_matches_device(sb):
     dev = ops.iradon(sino.cuda()).cpu()
     host = ops.iradon(sino.numpy())
     assert rel(np.asarray(host), dev.numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("algo,kind", [("sirt", "hamming"), ("cgls", "none"), ("tv", "none")])
+def test_solvers_fused_fft2_matches_cufft(sb, algo, kind):
+    """Solver grids (n = 512) go through the in-place fused FFT2 (TMA column
+    pass + bulk-copied row pass); the same solve with cuFFT's 2-D plan must
+    agree to the solver tolerance (1e-3) and run the same iterations."""
+    from oracle import shepp_logan
+    from paper_2003_12677_b200.solvers import solve_batch
+    ops = _ops(sb, 512, 96, kind)
+    sino = ops.radon(shepp_logan(512, 4).astype(np.float32))
+    cfg = sb.SolverConfig(algorithm=algo, max_iter=6)
+    rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    with _env("SPTB_NO_FUSED_FFT2", "1"):
+        rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    assert [r.iterations_run for r in rep] == [r.iterations_run for r in rep2]
+    assert rel(np.asarray(rec), np.asarray(rec2)) < 1e-3
