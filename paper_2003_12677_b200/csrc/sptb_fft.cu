@@ -695,6 +695,69 @@ k_fft2_col_tma(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ g,
     }
 }
 
+// Inverse FFT1 for radon with S^H rows in sample order: for angle t the P
+// rows t P + p of Q [s][b] are a P x B matrix whose columns are the batch
+// units, i.e. the y pass again with plane = angle and X = B.  N/256 TMA boxes
+// (4 columns x 256 rows) in, the column FFT, then the two real rows of each
+// unit (slices 2u, 2u + 1 at angle t, scaled by 1/P) leave by bulk stores from
+// a [2 c + h][P + 4] staging area (the +4 row pad spreads the 4 columns over
+// distinct banks).
+template <int LOGN>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1024 / (CW2 * (1 << LOGN) / 16))
+k_fft1_inv_col(const __grid_constant__ CUtensorMap tmap, int T, float scale, float* __restrict__ out, long long n,
+               long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3, RS = N + 4;
+    extern __shared__ __align__(128) unsigned char colbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(colbuf_raw);
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    const int b0 = blockIdx.x * CW2, t = blockIdx.y;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"((unsigned)(N * CW2 * sizeof(float2))) : "memory");
+#pragma unroll 1
+        for (int k = 0; k < N / 256; ++k)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(fbuf + k * 256 * CW2)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(b0), "r"(t * N + 256 * k), "r"(sb)
+                : "memory");
+    }
+    __syncthreads();
+    fbar_wait(sb, 0);
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
+    __syncthreads();
+    dft16<true>(v);
+    fft16_stages<LOGN, true>(v, fbuf + c * LD, j, tw);
+    __syncthreads();
+    float* stg = reinterpret_cast<float*>(fbuf);  // [2 CW2][RS]
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int pidx = j + TP * m;
+        const float2 z = v[(m % NB3) * R3 + m / NB3];
+        stg[(2 * c) * RS + pidx] = z.x * scale;
+        stg[(2 * c + 1) * RS + pidx] = z.y * scale;
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const long long plane = (long long)T * N;
+        for (int cc = 0; cc < CW2; ++cc) {
+            if (b0 + cc >= nb) break;
+            const long long u = u0 + b0 + cc;
+            bulk_s2g(out + (2 * u) * plane + (long long)t * N, stg + (2 * cc) * RS, N * 4u);
+            if (2 * u + 1 < n) bulk_s2g(out + (2 * u + 1) * plane + (long long)t * N, stg + (2 * cc + 1) * RS, N * 4u);
+        }
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+}
+
 // radon side: caller real pairs (slices 2u, 2u + 1) times deapo(y, x) ->
 // forward FFT along x -> G row (planes b >= nb are zero-filled: the S^H
 // kernel reads all B planes)
@@ -1267,6 +1330,45 @@ bool fft2_inplace_ok(const sptb_plan* p, const void* g) {
 
 int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st) {
     return inverse ? fft2_inplace<true>(p, (float2*)g, nb, st) : fft2_inplace<false>(p, (float2*)g, nb, st);
+}
+
+bool fft1_inv_tma_ok(const sptb_plan* p, const void* q, const void* out, int fmt, int B) {
+    return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->P) > 0 &&
+           B % CW2 == 0 && col_tma_ok(q) && ((uintptr_t)out % 16) == 0 &&
+           !getenv("SPTB_NO_FUSED_FFT1") && !getenv("SPTB_FFT1_INV_GATHER");
+}
+
+template <int LOGN>
+int inv_col_launch(sptb_plan* p, const void* q, int B, void* out, int64_t n, int64_t u0, int nb, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft1: twiddle table");
+    CUtensorMap tm;
+    const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)p->N};
+    const cuuint64_t strides[1] = {(cuuint64_t)B * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)CW2, 256u};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult cr = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(q), dims, strides, box,
+                                       es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SPTB_ERR_CUDA, "cuTensorMapEncodeTiled (fft1) failed: " + std::to_string((int)cr));
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    SPTB_CUDA(set_smem_once((const void*)k_fft1_inv_col<LOGN>, sm, SPTB_FFT_CARVEOUT));
+    k_fft1_inv_col<LOGN><<<dim3((unsigned)((nb + CW2 - 1) / CW2), (unsigned)p->T), NT, sm, st>>>(
+        tm, p->T, 1.0f / (float)p->P, (float*)out, n, u0, nb, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+int launch_fft1_inv_tma(sptb_plan* p, const void* q, int B, void* out, int64_t n, int64_t u0, int nb,
+                        cudaStream_t st) {
+    switch (log2_fft(p->P)) {
+        case 9: return inv_col_launch<9>(p, q, B, out, n, u0, nb, st);
+        case 10: return inv_col_launch<10>(p, q, B, out, n, u0, nb, st);
+        case 11: return inv_col_launch<11>(p, q, B, out, n, u0, nb, st);
+        case 12: return inv_col_launch<12>(p, q, B, out, n, u0, nb, st);
+    }
+    return fail(SPTB_ERR_ARG, "fft1 (TMA): unsupported n_p");
 }
 
 }  // namespace sptb

@@ -240,10 +240,12 @@ int launch_spmm(const DevCSR& A, const void* val, const void* x, void* y, int B,
 template <typename R>
 int launch_transpose_bm_to_mb(const void* in, void* out, int B, int64_t M, cudaStream_t st);
 
-// patch-grouped S^H: x [b][m] (batch-outer) -> y [s'][b]; sub: y = sub - S^H x
+// patch-grouped S^H: x [b][m] (batch-outer) -> y [s'][b]; sub: y = sub - S^H x;
+// sample_order: rows written at order[s'] = s instead (TMA path, no sub)
 template <typename R>
 int launch_spmm_sh_patch(const sptb_plan* p, const void* x_bm, void* y_sb, int B, const void* sub,
-                         cudaStream_t st);
+                         cudaStream_t st, bool sample_order = false);
+bool tma_ok(const sptb_plan* p, const void* x);  // the TMA S^H path is usable for operand x
 // [b][s] -> [perm[s]][b]   and   [s'][b] -> [b][order[s']]
 template <typename R>
 int launch_transpose_permute(const void* in_bs, void* out_sb, const int* perm, int B, int64_t N,
@@ -276,6 +278,10 @@ int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0
                     cudaStream_t st, bool permute = true);
 int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                     cudaStream_t st);
+// inverse FFT1 of rows in sample order (q [s][b]) staged by TMA -> caller real pairs
+bool fft1_inv_tma_ok(const sptb_plan* p, const void* q, const void* out, int fmt, int B);
+int launch_fft1_inv_tma(sptb_plan* p, const void* q, int B, void* out, int64_t n, int64_t u0, int nb,
+                        cudaStream_t st);
 // 2-D inverse FFT of G [b][y][x] (in place along y) fused with the
 // deapodization and unpack to caller real slice pairs (sptb_fft.cu)
 bool fft2_fused_ok(const sptb_plan* p, int fmt);

@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(256)
 k_sh_rows(const int* __restrict__ order, const int* __restrict__ rp, const int* __restrict__ col,
           const typename PCplx<R>::T* __restrict__ val, long long r_begin, long long N, int B,
           long long M, const typename PCplx<R>::T* __restrict__ x,
-          typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub) {
+          typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub,
+          int sample_order) {
     using C = typename PCplx<R>::T;
     const long long n = (N - r_begin) * B;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
@@ -414,7 +415,7 @@ k_sh_rows(const int* __restrict__ order, const int* __restrict__ rp, const int* 
             a.y = fma(v.x, xv.y, a.y);
             a.y = fma(v.y, xv.x, a.y);
         }
-        const size_t o = (size_t)r * B + b;
+        const size_t o = (size_t)(sample_order ? s : r) * B + b;
         if (SUB) {
             const C sv = sub[o];
             a.x = sv.x - a.x;
@@ -453,7 +454,8 @@ template <typename R, int G, int CPL, bool SUB>
 __global__ void __launch_bounds__(PT, SPTB_TMA_MINB)
 k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ items,
          const unsigned char* __restrict__ item_perm, const typename PCplx<R>::T* __restrict__ sval, int npx,
-         typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub) {
+         typename PCplx<R>::T* __restrict__ y, const typename PCplx<R>::T* __restrict__ sub,
+         const int* __restrict__ rowmap) {
     using C = typename PCplx<R>::T;
     constexpr int BB = G * CPL, NG = PT / G;
     constexpr int XS_BYTES = (BB * TMA_PS * (int)sizeof(C) + 127) & ~127;
@@ -539,7 +541,8 @@ k_sh_tma(const __grid_constant__ CUtensorMap tmap, const int4* __restrict__ item
                 acc[q] = a;
             }
         }
-        const size_t o = (size_t)(r0 + r) * BB;
+        // rowmap (order: s' -> s): rows in sample order for the fused inverse FFT1
+        const size_t o = (size_t)(rowmap ? __ldg(rowmap + r0 + r) : r0 + r) * BB;
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
             C out = acc[q];
@@ -566,14 +569,15 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {  // shared with sptb_fft.cu
 }
 
 // TMA path usable: 16-byte aligned operand and row/plane strides
-static bool tma_ok(const sptb_plan* p, const void* x) {
+bool tma_ok(const sptb_plan* p, const void* x) {
     const size_t cs = p->csize;
     return p->shp.slot_mode && tmap_encoder() != nullptr && ((uintptr_t)x % 16) == 0 &&
            ((size_t)p->X * cs) % 16 == 0 && ((size_t)p->M * cs) % 16 == 0 && !getenv("SPTB_NO_TMA");
 }
 
 template <typename R, int G, int CPL>
-static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const void* sub, cudaStream_t st) {
+static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const void* sub, cudaStream_t st,
+                           bool sample_order) {
     using C = typename PCplx<R>::T;
     const PatchSH& sp = p->shp;
     constexpr int BB = G * CPL;
@@ -594,7 +598,7 @@ static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const voi
         auto run = [&](auto kern) -> int {
             SPTB_CUDA(set_smem_once((const void*)kern, (int)sm));
             kern<<<(unsigned)sp.n_items, PT, sm, st>>>(tm, sp.items, sp.item_perm, (const C*)sp.sval, sp.npx,
-                                                       (C*)y, (const C*)sub);
+                                                       (C*)y, (const C*)sub, sample_order ? sp.order : nullptr);
             SPTB_LAUNCHED();
             return SPTB_OK;
         };
@@ -606,10 +610,10 @@ static int sh_tma_dispatch(const sptb_plan* p, const void* x, void* y, const voi
         const unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 8);
         if (sub)
             k_sh_rows<R, true><<<grid, 256, 0, st>>>(sp.order, p->SH.row_ptr, p->SH.col, (const C*)p->SH.val,
-                                                     sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub);
+                                                     sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub, sample_order ? 1 : 0);
         else
             k_sh_rows<R, false><<<grid, 256, 0, st>>>(sp.order, p->SH.row_ptr, p->SH.col, (const C*)p->SH.val,
-                                                      sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub);
+                                                      sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub, sample_order ? 1 : 0);
         SPTB_LAUNCHED();
     }
     return SPTB_OK;
@@ -651,10 +655,10 @@ static int sh_slot_dispatch(const sptb_plan* p, const void* x, void* y, const vo
         const unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 8);
         if (sub)
             k_sh_rows<R, true><<<grid, 256, 0, st>>>(sp.order, p->SH.row_ptr, p->SH.col, (const C*)p->SH.val,
-                                                     sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub);
+                                                     sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub, 0);
         else
             k_sh_rows<R, false><<<grid, 256, 0, st>>>(sp.order, p->SH.row_ptr, p->SH.col, (const C*)p->SH.val,
-                                                      sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub);
+                                                      sp.n_reg, p->N, BB, p->M, (const C*)x, (C*)y, (const C*)sub, 0);
         SPTB_LAUNCHED();
     }
     return SPTB_OK;
@@ -702,15 +706,17 @@ static int sh_patch_dispatch(const sptb_plan* p, const void* x, void* y, const v
 }
 template <typename R>
 int launch_spmm_sh_patch(const sptb_plan* p, const void* x_bm, void* y_sb, int B, const void* sub,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool sample_order) {
+    if (sample_order && (sub || !tma_ok(p, x_bm)))
+        return fail(SPTB_ERR_STATE, "patch spmm: sample-order output needs the TMA path");
     if (tma_ok(p, x_bm)) switch (B) {
-        case 1: return sh_tma_dispatch<R, 1, 1>(p, x_bm, y_sb, sub, st);
-        case 2: return sh_tma_dispatch<R, 2, 1>(p, x_bm, y_sb, sub, st);
-        case 4: return sh_tma_dispatch<R, 4, 1>(p, x_bm, y_sb, sub, st);
-        case 8: return sh_tma_dispatch<R, 8, 1>(p, x_bm, y_sb, sub, st);
-        case 16: return sh_tma_dispatch<R, 8, 2>(p, x_bm, y_sb, sub, st);
-        case 32: return sh_tma_dispatch<R, 8, 4>(p, x_bm, y_sb, sub, st);
-        case 64: return sh_tma_dispatch<R, 8, 8>(p, x_bm, y_sb, sub, st);
+        case 1: return sh_tma_dispatch<R, 1, 1>(p, x_bm, y_sb, sub, st, sample_order);
+        case 2: return sh_tma_dispatch<R, 2, 1>(p, x_bm, y_sb, sub, st, sample_order);
+        case 4: return sh_tma_dispatch<R, 4, 1>(p, x_bm, y_sb, sub, st, sample_order);
+        case 8: return sh_tma_dispatch<R, 8, 1>(p, x_bm, y_sb, sub, st, sample_order);
+        case 16: return sh_tma_dispatch<R, 8, 2>(p, x_bm, y_sb, sub, st, sample_order);
+        case 32: return sh_tma_dispatch<R, 8, 4>(p, x_bm, y_sb, sub, st, sample_order);
+        case 64: return sh_tma_dispatch<R, 8, 8>(p, x_bm, y_sb, sub, st, sample_order);
         default: return fail(SPTB_ERR_ARG, "patch spmm: batch must be a power of two <= 64");
     }
     if (p->shp.slot_mode) switch (B) {
@@ -734,8 +740,8 @@ int launch_spmm_sh_patch(const sptb_plan* p, const void* x_bm, void* y_sb, int B
     }
     return fail(SPTB_ERR_ARG, "patch spmm: batch must be a power of two <= 64");
 }
-template int launch_spmm_sh_patch<float>(const sptb_plan*, const void*, void*, int, const void*, cudaStream_t);
-template int launch_spmm_sh_patch<double>(const sptb_plan*, const void*, void*, int, const void*, cudaStream_t);
+template int launch_spmm_sh_patch<float>(const sptb_plan*, const void*, void*, int, const void*, cudaStream_t, bool);
+template int launch_spmm_sh_patch<double>(const sptb_plan*, const void*, void*, int, const void*, cudaStream_t, bool);
 
 // ---------------------------------------------------------------------------
 // Sample-axis transposes with the patch renumbering:

@@ -243,8 +243,11 @@ int radon_batch(sptb_plan* p, const void* in, int in_fmt, int64_t n, int64_t u0,
         SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->M, p->deapo, p->G0, st));
         SPTB_TRY(exec_fft(p, f->fft2, p->G0, CUFFT_FORWARD));
     }
-    // patch SpMM reads the batch-outer FFT2 output directly -> [s'][b]
-    SPTB_TRY(launch_spmm_sh_patch<R>(p, p->G0, p->S1, B, nullptr, st));
+    // patch SpMM reads the batch-outer FFT2 output directly -> [s'][b], or
+    // [s][b] (sample order) for the TMA-staged inverse FFT1
+    const bool so = tma_ok(p, p->G0) && fft1_inv_tma_ok(p, p->S1, out, out_fmt, B);
+    SPTB_TRY(launch_spmm_sh_patch<R>(p, p->G0, p->S1, B, nullptr, st, so));
+    if (so) return launch_fft1_inv_tma(p, p->S1, B, out, on, ou0, nb, st);
     if (fft1_fused_ok(p, out_fmt, B))  // gather [s'][b] + IFFT1 + unpack in one pass
         return launch_fft1_inv(p, p->S1, B, out, out_fmt, on, ou0, nb, st);
     SPTB_TRY(launch_transpose_unpermute<R>(p->S1, p->S0, p->shp.order, B, p->N, st));
