@@ -758,6 +758,70 @@ k_fft1_inv_col(const __grid_constant__ CUtensorMap tmap, int T, float scale, flo
     }
 }
 
+// Forward FFT1 for gridrec as a column pass: for angle t, the 2 CW2 real rows
+// (slices 2u, 2u + 1 of units b0..b0+3) come in by bulk copies into a
+// [2 c + h][P + 4] staging area, lane (c, j) runs the column FFT of unit
+// b0 + c, and Q rows t P + p (sample order) leave as N/256 TMA boxes of
+// 4 columns x 256 rows from [p][c] staging (the per-row 32-byte STG runs of
+// k_fft1r_fwd were its bottleneck).
+template <int LOGN>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1024 / (CW2 * (1 << LOGN) / 16))
+k_fft1_fwd_col(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ in, int T, long long n,
+               long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3, RS = N + 4;
+    extern __shared__ __align__(128) unsigned char colbuf_raw[];
+    float2* fbuf = reinterpret_cast<float2*>(colbuf_raw);
+    float* stg = reinterpret_cast<float*>(fbuf);  // [2 CW2][RS]
+    __shared__ __align__(8) unsigned long long bar;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar);
+    const int b0 = blockIdx.x * CW2, t = blockIdx.y;
+    const long long plane = (long long)T * N;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        unsigned bytes = 0;
+        for (int k = 0; k < 2 * CW2; ++k)
+            if (b0 + k / 2 < nb && 2 * (u0 + b0) + k < n) bytes += N * 4u;
+        if (bytes) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(bytes) : "memory");
+            for (int k = 0; k < 2 * CW2; ++k) {
+                const long long sl = 2 * (u0 + b0) + k;
+                if (b0 + k / 2 < nb && sl < n) bulk_g2s(stg + k * RS, in + sl * plane + (long long)t * N, N * 4u, sb);
+            }
+        }
+    }
+    __syncthreads();
+    if (b0 < nb) fbar_wait(sb, 0);  // some row was requested iff unit b0 is valid
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    const long long u = u0 + b0 + c;
+    const bool ha = b0 + c < nb, hb = ha && 2 * u + 1 < n;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const int i = j + TP * r;
+        v[r] = make_float2(ha ? stg[(2 * c) * RS + i] : 0.f, hb ? stg[(2 * c + 1) * RS + i] : 0.f);
+    }
+    __syncthreads();
+    dft16<false>(v);
+    fft16_stages<LOGN, false>(v, fbuf + c * LD, j, tw);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+        for (int k = 0; k < N / 256; ++k)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                    reinterpret_cast<unsigned long long>(&tmap)),
+                "r"(b0), "r"(t * N + 256 * k), "r"((unsigned)__cvta_generic_to_shared(fbuf + k * 256 * CW2))
+                : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+}
+
 // radon side: caller real pairs (slices 2u, 2u + 1) times deapo(y, x) ->
 // forward FFT along x -> G row (planes b >= nb are zero-filled: the S^H
 // kernel reads all B planes)
@@ -1338,19 +1402,58 @@ bool fft1_inv_tma_ok(const sptb_plan* p, const void* q, const void* out, int fmt
            !getenv("SPTB_NO_FUSED_FFT1") && !getenv("SPTB_FFT1_INV_GATHER");
 }
 
+// Q [s][b] complex64 (s in sample order) as a 2-D tensor of 8-byte elements;
+// box CW2 columns x 256 rows
+int q_tmap(const sptb_plan* p, const void* q, int B, CUtensorMap* tm) {
+    const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)p->N};
+    const cuuint64_t strides[1] = {(cuuint64_t)B * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)CW2, 256u};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult cr = tmap_encoder()(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(q), dims, strides, box,
+                                       es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SPTB_ERR_CUDA, "cuTensorMapEncodeTiled (fft1) failed: " + std::to_string((int)cr));
+    return SPTB_OK;
+}
+
+template <int LOGN>
+int fwd_col_launch(sptb_plan* p, const void* in, int64_t n, int64_t u0, int nb, int B, void* q, cudaStream_t st) {
+    const float2* tw = twiddles(p, LOGN);
+    if (!tw) return fail(SPTB_ERR_CUDA, "fft1: twiddle table");
+    CUtensorMap tm;
+    SPTB_TRY(q_tmap(p, q, B, &tm));
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd_col<LOGN>, sm, SPTB_FFT_CARVEOUT));
+    k_fft1_fwd_col<LOGN><<<dim3((unsigned)(B / CW2), (unsigned)p->T), NT, sm, st>>>(tm, (const float*)in, p->T, n, u0,
+                                                                                   nb, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
+int launch_fft1_fwd_tma(sptb_plan* p, const void* in, int64_t n, int64_t u0, int nb, int B, void* q,
+                        cudaStream_t st) {
+    switch (log2_fft(p->P)) {
+        case 9: return fwd_col_launch<9>(p, in, n, u0, nb, B, q, st);
+        case 10: return fwd_col_launch<10>(p, in, n, u0, nb, B, q, st);
+        case 11: return fwd_col_launch<11>(p, in, n, u0, nb, B, q, st);
+        case 12: return fwd_col_launch<12>(p, in, n, u0, nb, B, q, st);
+    }
+    return fail(SPTB_ERR_ARG, "fft1 (TMA): unsupported n_p");
+}
+
+bool fft1_fwd_tma_ok(const sptb_plan* p, const void* in, const void* q, int fmt, int B) {
+    return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->P) > 0 &&
+           B % CW2 == 0 && col_tma_ok(q) && ((uintptr_t)in % 16) == 0 && !getenv("SPTB_NO_FUSED_FFT1") &&
+           !getenv("SPTB_FFT1_FWD_ROWS");
+}
+
 template <int LOGN>
 int inv_col_launch(sptb_plan* p, const void* q, int B, void* out, int64_t n, int64_t u0, int nb, cudaStream_t st) {
     const float2* tw = twiddles(p, LOGN);
     if (!tw) return fail(SPTB_ERR_CUDA, "fft1: twiddle table");
     CUtensorMap tm;
-    const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)p->N};
-    const cuuint64_t strides[1] = {(cuuint64_t)B * 8};
-    const cuuint32_t box[2] = {(cuuint32_t)CW2, 256u};
-    const cuuint32_t es[2] = {1, 1};
-    const CUresult cr = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(q), dims, strides, box,
-                                       es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) return fail(SPTB_ERR_CUDA, "cuTensorMapEncodeTiled (fft1) failed: " + std::to_string((int)cr));
+    SPTB_TRY(q_tmap(p, q, B, &tm));
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
     SPTB_CUDA(set_smem_once((const void*)k_fft1_inv_col<LOGN>, sm, SPTB_FFT_CARVEOUT));

@@ -278,6 +278,10 @@ int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0
                     cudaStream_t st, bool permute = true);
 int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                     cudaStream_t st);
+// forward FFT1 of caller real pairs -> q [s][b] (sample order) by TMA stores
+bool fft1_fwd_tma_ok(const sptb_plan* p, const void* in, const void* q, int fmt, int B);
+int launch_fft1_fwd_tma(sptb_plan* p, const void* in, int64_t n, int64_t u0, int nb, int B, void* q,
+                        cudaStream_t st);
 // inverse FFT1 of rows in sample order (q [s][b]) staged by TMA -> caller real pairs
 bool fft1_inv_tma_ok(const sptb_plan* p, const void* q, const void* out, int fmt, int B);
 int launch_fft1_inv_tma(sptb_plan* p, const void* q, int B, void* out, int64_t n, int64_t u0, int nb,

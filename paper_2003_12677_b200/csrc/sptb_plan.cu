@@ -266,7 +266,10 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     if (fft1_fused_ok(p, in_fmt, B) && !getenv("SPTB_FFT1_PERM")) {
         // pack + FFT1 in one pass, rows left in sample order: the row gather
         // of S reads them through its original column indices (no permutation)
-        SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st, false));
+        if (fft1_fwd_tma_ok(p, in, p->S1, in_fmt, B))
+            SPTB_TRY(launch_fft1_fwd_tma(p, in, n, u0, nb, B, p->S1, st));
+        else
+            SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st, false));
         SPTB_TRY(launch_spmm<R>(p->S, vals, p->S1, p->G0, B, true, nullptr, st));
     } else {
         if (fft1_fused_ok(p, in_fmt, B)) {  // pack + FFT1 + permute in one pass

@@ -60,13 +60,16 @@ def test_fused_fft1_matches_cufft_path(sb, n, T):
     rec_fast, sin_fast = ops.iradon(sino), ops.radon(img)
     with _env("SPTB_NO_FUSED_FFT1", "1"):
         rec_ref, sin_ref = ops.iradon(sino), ops.radon(img)
-    with _env("SPTB_FFT1_NO_BULK", "1"):  # per-lane loads instead of bulk-copied rows
-        rec_lanes = ops.iradon(sino)
+    with _env("SPTB_FFT1_FWD_ROWS", "1"):  # row-FFT kernel instead of the TMA column pass
+        rec_rows = ops.iradon(sino)
+        with _env("SPTB_FFT1_NO_BULK", "1"):  # ... with per-lane loads
+            rec_lanes = ops.iradon(sino)
     with _env("SPTB_FFT1_INV_GATHER", "1"):  # S^H in patch order + gathering inverse FFT1
         sin_gather = ops.radon(img)
     torch.cuda.synchronize()
     assert rel(sin_fast.cpu().numpy(), sin_gather.cpu().numpy()) < 1e-6
     assert rel(rec_fast.cpu().numpy(), rec_ref.cpu().numpy()) < 1e-5
+    assert rel(rec_fast.cpu().numpy(), rec_rows.cpu().numpy()) < 1e-6
     assert rel(rec_fast.cpu().numpy(), rec_lanes.cpu().numpy()) < 1e-6
     assert rel(sin_fast.cpu().numpy(), sin_ref.cpu().numpy()) < 1e-5
 
