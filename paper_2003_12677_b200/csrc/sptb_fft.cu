@@ -695,6 +695,77 @@ k_fft2_col_tma(const __grid_constant__ CUtensorMap tmap, float2* __restrict__ g,
     }
 }
 
+// Persistent y pass: one 512-thread CTA per SM walks strips blockIdx.x,
+// + gridDim.x, ... with three strip buffers: while strip k is transformed in
+// buffer k % 3, strip k + 1 is already loading into the next buffer and
+// strip k - 1's TMA store drains from the previous one (ncu: the per-strip
+// kernel spent ~50% of its warps' time waiting for its own load).
+constexpr int COLP_BUFS = 3;
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1)
+k_fft2_col_pers(const __grid_constant__ CUtensorMap tmap, int strips, int nstrip, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3;
+    constexpr int BUF = CW2 * LD;  // float2 per buffer (>= N * CW2 staging)
+    extern __shared__ __align__(128) unsigned char colpbuf_raw[];
+    float2* base = reinterpret_cast<float2*>(colpbuf_raw);
+    __shared__ __align__(8) unsigned long long bar[COLP_BUFS];
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    auto load = [&](int s, int k) {  // tid 0: strip s into buffer k % 3
+        const int b = s / strips, x0 = (s - b * strips) * CW2;
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        float2* dst = base + (k % COLP_BUFS) * BUF;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"((unsigned)(N * CW2 * sizeof(float2))) : "memory");
+#pragma unroll 1
+        for (int q = 0; q < N / 256; ++q)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst + q * 256 * CW2)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(x0), "r"(256 * q), "r"(b), "r"(sb)
+                : "memory");
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < COLP_BUFS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    int k = 0;
+    for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
+        float2* fbuf = base + (k % COLP_BUFS) * BUF;
+        if (threadIdx.x == 0 && s + (int)gridDim.x < nstrip) {
+            // buffer (k + 1) % 3 last held strip k - 2: its store must have been read out
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(s + gridDim.x, k + 1);
+        }
+        fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
+        __syncthreads();
+        dft16<INV>(v);
+        fft16_stages<LOGN, INV>(v, fbuf + c * LD, j, tw);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int b = s / strips, x0 = (s - b * strips) * CW2;
+#pragma unroll 1
+            for (int q = 0; q < N / 256; ++q)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                        reinterpret_cast<unsigned long long>(&tmap)),
+                    "r"(x0), "r"(256 * q), "r"(b), "r"((unsigned)__cvta_generic_to_shared(fbuf + q * 256 * CW2))
+                    : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 // Inverse FFT1 for radon with S^H rows in sample order: for angle t the P
 // rows t P + p of Q [s][b] are a P x B matrix whose columns are the batch
 // units, i.e. the y pass again with plane = angle and X = B.  N/256 TMA boxes
@@ -1071,6 +1142,36 @@ int col_tmap(const sptb_plan* p, const void* g, int planes, CUtensorMap* tm) {
     return SPTB_OK;
 }
 
+int sm_count() {
+    static int n = [] {
+        int d = 0, v = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        return v;
+    }();
+    return n;
+}
+
+// y pass over nb planes: persistent triple-buffered kernel (default) or one CTA per strip
+template <int LOGN, bool INV>
+int run_col(const CUtensorMap& tm, float2* g, int X, long long M, int strips, int nb, const float2* tw,
+            cudaStream_t st) {
+    constexpr int NT = CW2 * (1 << LOGN) / 16;
+    const int nstrip = nb * strips;
+    const size_t buf = sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2);
+    if (COLP_BUFS * buf <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+        const int sm = (int)(COLP_BUFS * buf);
+        SPTB_CUDA(set_smem_once((const void*)k_fft2_col_pers<LOGN, INV>, sm, SPTB_FFT_CARVEOUT));
+        k_fft2_col_pers<LOGN, INV><<<(unsigned)std::min(nstrip, sm_count()), NT, sm, st>>>(tm, strips, nstrip, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
+    SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, INV>, (int)buf, SPTB_FFT_CARVEOUT));
+    k_fft2_col_tma<LOGN, INV><<<(unsigned)nstrip, NT, (int)buf, st>>>(tm, g, X, M, strips, tw);
+    SPTB_LAUNCHED();
+    return SPTB_OK;
+}
+
 template <int LOGN>
 int col_launch(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     const float2* tw = twiddles(p, LOGN);
@@ -1081,10 +1182,7 @@ int col_launch(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     if (col_tma_ok(g)) {
         CUtensorMap tm;
         SPTB_TRY(col_tmap(p, g, nb, &tm));
-        SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
-        k_fft2_col_tma<LOGN, true><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
-        SPTB_LAUNCHED();
-        return SPTB_OK;
+        return run_col<LOGN, true>(tm, g, p->X, p->M, strips, nb, tw, st);
     }
     SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, true>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_col<LOGN, true><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
@@ -1102,10 +1200,7 @@ int col_launch_fwd(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     if (col_tma_ok(g)) {
         CUtensorMap tm;
         SPTB_TRY(col_tmap(p, g, nb, &tm));
-        SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
-        k_fft2_col_tma<LOGN, false><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
-        SPTB_LAUNCHED();
-        return SPTB_OK;
+        return run_col<LOGN, false>(tm, g, p->X, p->M, strips, nb, tw, st);
     }
     SPTB_CUDA(set_smem_once((const void*)k_fft2_col<LOGN, false>, sm, SPTB_FFT_CARVEOUT));
     k_fft2_col<LOGN, false><<<(unsigned)(nb * strips), NT, sm, st>>>(g, p->X, p->M, strips, tw);
@@ -1129,10 +1224,7 @@ int col_launch_dir(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
     const int strips = p->X / CW2;
     CUtensorMap tm;
     SPTB_TRY(col_tmap(p, g, nb, &tm));
-    SPTB_CUDA(set_smem_once((const void*)k_fft2_col_tma<LOGN, INV>, sm, SPTB_FFT_CARVEOUT));
-    k_fft2_col_tma<LOGN, INV><<<(unsigned)(nb * strips), NT, sm, st>>>(tm, g, p->X, p->M, strips, tw);
-    SPTB_LAUNCHED();
-    return SPTB_OK;
+    return run_col<LOGN, INV>(tm, g, p->X, p->M, strips, nb, tw, st);
 }
 
 template <int LOGN, bool INV>
