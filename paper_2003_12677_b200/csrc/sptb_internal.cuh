@@ -293,6 +293,9 @@ int launch_fft2_inv_unpack(sptb_plan* p, void* g, const void* plane, double scal
                            int64_t u0, int nb, cudaStream_t st);
 // in-place unnormalised 2-D FFT of nb planes (solver grids), complex64 only
 bool fft2_inplace_ok(const sptb_plan* p, const void* g);
+const float2* fft2_twiddles(sptb_plan* p, int logn);
+int fft2_log2(long long n);  // log2 n for 512 <= n = 2^k <= 4096, else 0
+int launch_fft2_cols(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st);
 int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st);
 // caller real pairs times plane -> forward 2-D FFT -> G [b][y][x], B planes
 int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_t n, int64_t u0, int nb, int B,

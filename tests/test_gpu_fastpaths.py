@@ -165,3 +165,8 @@ def test_solvers_fused_fft2_matches_cufft(sb, algo, kind):
         rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
     assert [r.iterations_run for r in rep] == [r.iterations_run for r in rep2]
     assert rel(np.asarray(rec), np.asarray(rec2)) < 1e-3
+    if algo == "sirt":  # update + x pass fused vs OpSirtUpdate and the separate FFT2
+        with _env("SPTB_SIRT_UNFUSED", "1"):
+            rec3, rep3, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+        assert [r.iterations_run for r in rep] == [r.iterations_run for r in rep3]
+        assert rel(np.asarray(rec), np.asarray(rec3)) < 1e-4
