@@ -277,6 +277,60 @@ k_sirt_update_rowfft(float2* __restrict__ u, const float2* __restrict__ g, float
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(bad_count + b, (double)bad);
 }
 
+// Inverse-FFT2 x pass fused with OpAdjPost<float, true> (SIRT's gradient):
+// W row -> IFFT_x -> g_new = deapo * scale * row; BB dots against the old g
+// (<go,go>, <go, go - gn> per channel) reduced per CTA in a fixed order and
+// written as part[(y0 / 4 * B + b) * 4 + k] for k_finish: deterministic.
+template <int LOGN>
+__global__ void __launch_bounds__(4 * (1 << LOGN) / 16, 1024 / (4 * (1 << LOGN) / 16))
+k_sirt_adjpost_rowfft(const float2* __restrict__ w, float2* __restrict__ g, const float* __restrict__ deapo,
+                      double scale, long long M, int Y, int B, const float2* __restrict__ tw,
+                      double* __restrict__ part) {
+    using namespace fftcore;
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, NT = 4 * TP;
+    extern __shared__ __align__(16) float2 sirt_fbuf[];
+    __shared__ double red[4][NT / 32];
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const long long gr0 = (long long)blockIdx.x * 4;
+    const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y), y = y0 + rb;
+    const size_t base = (size_t)b * M + (size_t)y * N;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = w[base + j + TP * r];
+    dft16<true>(v);
+    fft16_stages<LOGN, true>(v, sirt_fbuf + rb * N, j, tw);
+    double acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < NB3; ++q)
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const int x = j + TP * q + 256 * r;
+            const double d = (double)deapo[(size_t)y * N + x] * scale;
+            const float2 z = v[q * R3 + r];
+            const float2 gn = make_float2((float)(z.x * d), (float)(z.y * d));
+            const float2 go = g[base + x];
+            acc[0] += (double)go.x * go.x;
+            acc[1] += (double)go.y * go.y;
+            acc[2] += (double)go.x * ((double)go.x - (double)gn.x);
+            acc[3] += (double)go.y * ((double)go.y - (double)gn.y);
+            g[base + x] = gn;
+        }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double t = acc[k];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+        if (lane == 0) red[k][warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0;
+        for (int i = 0; i < NT / 32; ++i) t += red[threadIdx.x][i];
+        part[((size_t)(y0 / 4) * B + b) * 4 + threadIdx.x] = t;
+    }
+}
+
 template <typename R, typename V>
 struct OpDeapo {  // w = deapo * v * scale  (v of any precision, w of plan precision)
     using C = typename CT<R>::T;
@@ -1140,6 +1194,40 @@ struct Solver {
         }
     }
 
+    // S_(w) RH -> W, y pass, then the x pass fused with OpAdjPost<R, true> -> G, sums3
+    int sirt_adjoint_post(double scale) {
+        if constexpr (sizeof(R) == 4) {
+            const int L = fft2_log2(p->X);
+            const float2* tw = fft2_twiddles(p, L);
+            if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+            const void* vals = p->SW_val ? p->SW_val : p->S.val;
+            SPTB_TRY(launch_spmm_s<R>(p, vals, RH, W, B, st));
+            SPTB_TRY(launch_fft2_cols(p, W, B, true, st));
+            const unsigned grid = (unsigned)((long long)B * p->Y / 4);
+            auto run = [&](auto kern, int logn) -> int {
+                const int nt = 4 * (1 << logn) / 16, sm = (int)(sizeof(float2) * 4 * (1 << logn));
+                SPTB_CUDA(set_smem_once((const void*)kern, sm, -1));
+                kern<<<grid, nt, sm, st>>>((const float2*)W, (float2*)G, (const float*)p->deapo, scale, p->M, p->Y,
+                                           B, tw, part);
+                SPTB_LAUNCHED();
+                return SPTB_OK;
+            };
+            switch (L) {
+                case 9: SPTB_TRY(run(k_sirt_adjpost_rowfft<9>, 9)); break;
+                case 10: SPTB_TRY(run(k_sirt_adjpost_rowfft<10>, 10)); break;
+                case 11: SPTB_TRY(run(k_sirt_adjpost_rowfft<11>, 11)); break;
+                case 12: SPTB_TRY(run(k_sirt_adjpost_rowfft<12>, 12)); break;
+                default: return fail(SPTB_ERR_ARG, "sirt fused pass: unsupported n_x");
+            }
+            k_finish<<<(B * 4 * 32 + 255) / 256, 256, 0, st>>>(part, p->Y / 4, B, 4, 0, sums3);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        } else {
+            (void)scale;
+            return fail(SPTB_ERR_STATE, "sirt fused pass: complex64 only");
+        }
+    }
+
     // out[s][b] = (sub ? sub - : ) S^H FFT2(W)    (W holds deapo*v, [b][m]; clobbered)
     int forward_spec(C* out, const C* sub) {
         FFTPlans* f;
@@ -1230,8 +1318,12 @@ struct Solver {
             k_sirt_check<<<1, 64, 0, st>>>(us, sums, sums2, p->P, it, B, hist, cfg.tol);
             SPTB_TRY(unit_kernel_done());
             // g_new = A^H W r ; BB dots against the previous g
-            SPTB_TRY(adjoint_grid(RH, true));
-            SPTB_TRY(grid<4>(OpAdjPost<R, true>{W, G, deapo(), invP}, sums3));
+            if (sirt_fused_ok()) {
+                SPTB_TRY(sirt_adjoint_post(invP));
+            } else {
+                SPTB_TRY(adjoint_grid(RH, true));
+                SPTB_TRY(grid<4>(OpAdjPost<R, true>{W, G, deapo(), invP}, sums3));
+            }
             k_sirt_alpha<<<1, 64, 0, st>>>(us, sums3, B, cfg.bb_enabled);
             SPTB_TRY(unit_kernel_done());
         }
