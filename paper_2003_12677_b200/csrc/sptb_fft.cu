@@ -729,6 +729,83 @@ k_fft1_fwd_col(const __grid_constant__ CUtensorMap tmap, const float* __restrict
     }
 }
 
+// Persistent version of k_fft1_fwd_col (same triple-buffer scheme as
+// k_fft2_col_pers): strip s = (angle t, unit group bg), bg fastest.
+template <int LOGN>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1)
+k_fft1_fwd_pers(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ in, int T, int ngrp,
+                long long n, long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3, RS = N + 4;
+    constexpr int BUF = CW2 * LD;
+    extern __shared__ __align__(128) unsigned char colpbuf_raw[];
+    float2* base = reinterpret_cast<float2*>(colpbuf_raw);
+    __shared__ __align__(8) unsigned long long bar[COLP_BUFS];
+    const long long plane = (long long)T * N;
+    const int nstrip = ngrp * T;
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    auto load = [&](int s, int k) {  // tid 0: rows of strip s into buffer k % 3 (only valid units)
+        const int bg = s % ngrp, t = s / ngrp, b0 = bg * CW2;
+        if (b0 >= nb) return;
+        float* stg = reinterpret_cast<float*>(base + (k % COLP_BUFS) * BUF);
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        unsigned bytes = 0;
+        for (int q = 0; q < 2 * CW2; ++q)
+            if (b0 + q / 2 < nb && 2 * (u0 + b0) + q < n) bytes += N * 4u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(bytes) : "memory");
+        for (int q = 0; q < 2 * CW2; ++q) {
+            const long long sl = 2 * (u0 + b0) + q;
+            if (b0 + q / 2 < nb && sl < n) bulk_g2s(stg + q * RS, in + sl * plane + (long long)t * N, N * 4u, sb);
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < COLP_BUFS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    int k = 0;
+    for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
+        float2* fbuf = base + (k % COLP_BUFS) * BUF;
+        float* stg = reinterpret_cast<float*>(fbuf);
+        const int bg = s % ngrp, t = s / ngrp, b0 = bg * CW2;
+        if (threadIdx.x == 0 && s + (int)gridDim.x < nstrip) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(s + gridDim.x, k + 1);
+        }
+        // a group with no valid unit issued no copy and never arrives: only zeros
+        if (b0 < nb)
+            fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        const long long u = u0 + b0 + c;
+        const bool ha = b0 + c < nb, hb = ha && 2 * u + 1 < n;
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int i = j + TP * r;
+            v[r] = make_float2(ha ? stg[(2 * c) * RS + i] : 0.f, hb ? stg[(2 * c + 1) * RS + i] : 0.f);
+        }
+        __syncthreads();
+        dft16<false>(v);
+        fft16_stages<LOGN, false>(v, fbuf + c * LD, j, tw);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll 1
+            for (int q = 0; q < N / 256; ++q)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                        reinterpret_cast<unsigned long long>(&tmap)),
+                    "r"(b0), "r"(t * N + 256 * q), "r"((unsigned)__cvta_generic_to_shared(fbuf + q * 256 * CW2))
+                    : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 // radon side: caller real pairs (slices 2u, 2u + 1) times deapo(y, x) ->
 // forward FFT along x -> G row (planes b >= nb are zero-filled: the S^H
 // kernel reads all B planes)
@@ -1352,6 +1429,14 @@ int fwd_col_launch(sptb_plan* p, const void* in, int64_t n, int64_t u0, int nb, 
     SPTB_TRY(q_tmap(p, q, B, &tm));
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    if (COLP_BUFS * sm <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+        const int smp = COLP_BUFS * sm, nstrip = (B / CW2) * p->T;
+        SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
+        k_fft1_fwd_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
+            tm, (const float*)in, p->T, B / CW2, n, u0, nb, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
     SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd_col<LOGN>, sm, SPTB_FFT_CARVEOUT));
     k_fft1_fwd_col<LOGN><<<dim3((unsigned)(B / CW2), (unsigned)p->T), NT, sm, st>>>(tm, (const float*)in, p->T, n, u0,
                                                                                    nb, tw);
