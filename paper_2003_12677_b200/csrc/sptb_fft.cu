@@ -1016,6 +1016,82 @@ k_fft2_row_b(float2* __restrict__ g, const float2* __restrict__ tw) {
     }
 }
 
+// Persistent version of k_fft2_row_unpack_b: one 512-thread CTA per SM walks
+// 4-row strips with three 64 KB buffers (next strip's bulk load and the
+// previous strip's two bulk stores overlap the current FFT); the deapo x
+// factors are staged once.
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1)
+k_fft2_row_unpack_pers(const float2* __restrict__ g, long long M, int Y, const float* __restrict__ dxy, float scale,
+                       float* __restrict__ out, long long n, long long u0, int nstrip, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, BUF = RB2 * N;
+    extern __shared__ __align__(128) unsigned char rowpbuf_raw[];
+    float2* base = reinterpret_cast<float2*>(rowpbuf_raw);
+    float* fxs = reinterpret_cast<float*>(base + COLP_BUFS * BUF);
+    __shared__ __align__(8) unsigned long long bar[COLP_BUFS + 1];
+    auto load = [&](int s, int k) {
+        const long long gr0 = (long long)s * RB2;
+        const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(BUF * 8u) : "memory");
+        bulk_g2s(base + (k % COLP_BUFS) * BUF, g + (size_t)b * M + (size_t)y0 * N, BUF * 8u, sb);
+    };
+    const unsigned fb = (unsigned)__cvta_generic_to_shared(&bar[COLP_BUFS]);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i <= COLP_BUFS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if (dxy) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(N * 4u) : "memory");
+            bulk_g2s(fxs, dxy, N * 4u, fb);
+        }
+        if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    if (dxy) fbar_wait(fb, 0);
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    int k = 0;
+    for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
+        float2* fbuf = base + (k % COLP_BUFS) * BUF;
+        const long long gr0 = (long long)s * RB2;
+        const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+        if (threadIdx.x == 0 && s + (int)gridDim.x < nstrip) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(s + gridDim.x, k + 1);
+        }
+        fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = fbuf[rb * N + j + TP * r];
+        __syncthreads();
+        dft16<true>(v);
+        fft16_stages<LOGN, true>(v, fbuf + rb * N, j, tw);
+        __syncthreads();
+        float* sa = reinterpret_cast<float*>(fbuf);
+        float* sbm = sa + RB2 * N;
+        const Deapo dp(dxy, fxs, N, Y, y0 + rb, scale);
+#pragma unroll
+        for (int q = 0; q < NB3; ++q)
+#pragma unroll
+            for (int r = 0; r < R3; ++r) {
+                const int x = j + TP * q + 256 * r;
+                const float f = dp(x);
+                const float2 z = v[q * R3 + r];
+                sa[rb * N + x] = z.x * f;
+                sbm[rb * N + x] = z.y * f;
+            }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const long long u = u0 + b;
+            bulk_s2g(out + (size_t)(2 * u) * M + (size_t)y0 * N, sa, RB2 * N * 4u);
+            if (2 * u + 1 < n) bulk_s2g(out + (size_t)(2 * u + 1) * M + (size_t)y0 * N, sbm, RB2 * N * 4u);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 int log2_fft(long long n) {
     if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
     int l = 0;
@@ -1199,6 +1275,15 @@ int row_launch(sptb_plan* p, const float2* g, const float* plane, float scale, f
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = RB2 * (1 << LOGN) / 16;
     if (row_bulk_ok(out, g)) {
+        const int smp = (int)((COLP_BUFS * 8 * RB2 + 4) * (1 << LOGN));
+        if (smp <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+            const int nstrip = (int)((long long)nb * p->Y / RB2);
+            SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
+            k_fft2_row_unpack_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
+                g, p->M, p->Y, plane ? p->deapo_xy : nullptr, scale, out, n, u0, nstrip, tw);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
         const int smb = (int)((8 * RB2 + 4) * (1 << LOGN));
         SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack_b<LOGN>, smb, SPTB_FFT_CARVEOUT));
         k_fft2_row_unpack_b<LOGN><<<(unsigned)((long long)nb * p->Y / RB2), NT, smb, st>>>(
