@@ -1092,6 +1092,82 @@ k_fft2_row_unpack_pers(const float2* __restrict__ g, long long M, int Y, const f
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// Persistent version of k_fft1_inv_col: strip s = (angle t, group bg of
+// CW2 units with at least one valid unit), bg fastest; triple-buffered like
+// k_fft2_col_pers (TMA loads of Q boxes, bulk stores of the slice rows).
+template <int LOGN>
+__global__ void __launch_bounds__(CW2 * (1 << LOGN) / 16, 1)
+k_fft1_inv_pers(const __grid_constant__ CUtensorMap tmap, int T, int ngrp, float scale, float* __restrict__ out,
+                long long n, long long u0, int nb, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, LD = N + 16 / CW2, R3 = N / 256, NB3 = 16 / R3, RS = N + 4;
+    constexpr int BUF = CW2 * LD;
+    extern __shared__ __align__(128) unsigned char colpbuf_raw[];
+    float2* base = reinterpret_cast<float2*>(colpbuf_raw);
+    __shared__ __align__(8) unsigned long long bar[COLP_BUFS];
+    const int nstrip = ngrp * T;
+    const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
+    auto load = [&](int s, int k) {
+        const int bg = s % ngrp, t = s / ngrp;
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        float2* dst = base + (k % COLP_BUFS) * BUF;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"((unsigned)(N * CW2 * sizeof(float2))) : "memory");
+#pragma unroll 1
+        for (int q = 0; q < N / 256; ++q)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst + q * 256 * CW2)),
+                "l"(reinterpret_cast<unsigned long long>(&tmap)), "r"(bg * CW2), "r"(t * N + 256 * q), "r"(sb)
+                : "memory");
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < COLP_BUFS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    const long long plane = (long long)T * N;
+    int k = 0;
+    for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
+        float2* fbuf = base + (k % COLP_BUFS) * BUF;
+        const int bg = s % ngrp, t = s / ngrp, b0 = bg * CW2;
+        if (threadIdx.x == 0 && s + (int)gridDim.x < nstrip) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(s + gridDim.x, k + 1);
+        }
+        fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
+        __syncthreads();
+        dft16<true>(v);
+        fft16_stages<LOGN, true>(v, fbuf + c * LD, j, tw);
+        __syncthreads();
+        float* stg = reinterpret_cast<float*>(fbuf);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int pidx = j + TP * m;
+            const float2 z = v[(m % NB3) * R3 + m / NB3];
+            stg[(2 * c) * RS + pidx] = z.x * scale;
+            stg[(2 * c + 1) * RS + pidx] = z.y * scale;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int cc = 0; cc < CW2; ++cc) {
+                if (b0 + cc >= nb) break;
+                const long long u = u0 + b0 + cc;
+                bulk_s2g(out + (2 * u) * plane + (long long)t * N, stg + (2 * cc) * RS, N * 4u);
+                if (2 * u + 1 < n)
+                    bulk_s2g(out + (2 * u + 1) * plane + (long long)t * N, stg + (2 * cc + 1) * RS, N * 4u);
+            }
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 int log2_fft(long long n) {
     if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
     int l = 0;
@@ -1554,6 +1630,14 @@ int inv_col_launch(sptb_plan* p, const void* q, int B, void* out, int64_t n, int
     SPTB_TRY(q_tmap(p, q, B, &tm));
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
+    if (COLP_BUFS * sm <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+        const int smp = COLP_BUFS * sm, ngrp = (nb + CW2 - 1) / CW2, nstrip = ngrp * p->T;
+        SPTB_CUDA(set_smem_once((const void*)k_fft1_inv_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
+        k_fft1_inv_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
+            tm, p->T, ngrp, 1.0f / (float)p->P, (float*)out, n, u0, nb, tw);
+        SPTB_LAUNCHED();
+        return SPTB_OK;
+    }
     SPTB_CUDA(set_smem_once((const void*)k_fft1_inv_col<LOGN>, sm, SPTB_FFT_CARVEOUT));
     k_fft1_inv_col<LOGN><<<dim3((unsigned)((nb + CW2 - 1) / CW2), (unsigned)p->T), NT, sm, st>>>(
         tm, p->T, 1.0f / (float)p->P, (float*)out, n, u0, nb, tw);
