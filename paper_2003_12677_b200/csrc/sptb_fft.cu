@@ -745,9 +745,12 @@ k_fft1_fwd_pers(const __grid_constant__ CUtensorMap tmap, const float* __restric
     const int c = threadIdx.x % CW2, j = threadIdx.x / CW2;
     auto load = [&](int s, int k) {  // tid 0: rows of strip s into buffer k % 3 (only valid units)
         const int bg = s % ngrp, t = s / ngrp, b0 = bg * CW2;
-        if (b0 >= nb) return;
         float* stg = reinterpret_cast<float*>(base + (k % COLP_BUFS) * BUF);
         const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        if (b0 >= nb) {  // nothing to load: still complete the phase (parity is counted per use)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sb) : "memory");
+            return;
+        }
         unsigned bytes = 0;
         for (int q = 0; q < 2 * CW2; ++q)
             if (b0 + q / 2 < nb && 2 * (u0 + b0) + q < n) bytes += N * 4u;
@@ -773,9 +776,7 @@ k_fft1_fwd_pers(const __grid_constant__ CUtensorMap tmap, const float* __restric
             asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
             load(s + gridDim.x, k + 1);
         }
-        // a group with no valid unit issued no copy and never arrives: only zeros
-        if (b0 < nb)
-            fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
         const long long u = u0 + b0 + c;
         const bool ha = b0 + c < nb, hb = ha && 2 * u + 1 < n;
         float2 v[16];
@@ -1329,6 +1330,7 @@ int row_pack_launch(sptb_plan* p, const float* in, const float* plane, int64_t n
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = RB2 * (1 << LOGN) / 16;
     if (row_bulk_ok(in, g)) {
+        // (a persistent triple-buffered version measured 0.477 vs 0.467 ms: not used)
         const int smb = (int)((8 * RB2 + 4) * (1 << LOGN));
         SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack_b<LOGN>, smb, SPTB_FFT_CARVEOUT));
         k_fft2_row_pack_b<LOGN><<<(unsigned)((long long)B * p->Y / RB2), NT, smb, st>>>(
