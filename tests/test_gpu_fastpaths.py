@@ -188,3 +188,23 @@ def test_partial_batches_through_persistent_passes(sb, nslices):
     torch.cuda.synchronize()
     assert rel(fast.cpu().numpy(), ref.cpu().numpy()) < 1e-6
     assert rel(fast_s.cpu().numpy(), ref_s.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("n,T,nx,ny", [(4096, 6, None, None), (1024, 24, 512, 2048), (512, 45, 1024, 512)])
+def test_sirt_fused_passes_other_grids(sb, n, T, nx, ny):
+    """The fused SIRT x passes at 4096-wide rows (1024-thread CTAs) and on
+    rectangular grids vs the unfused element passes + FFT2."""
+    import torch
+    from paper_2003_12677_b200.solvers import solve_batch
+    ops = sb.build_operators(sb.ScanGeometry(n_p=n, n_theta=T, n_x=nx, n_y=ny), filter_kind="hamming",
+                             max_batch=4)
+    g = torch.Generator(device="cuda").manual_seed(n + T)
+    img = torch.rand(4, ops.geom.n_y, ops.geom.n_x, device="cuda", generator=g)
+    sino = ops.radon(img)
+    cfg = sb.SolverConfig(algorithm="sirt", max_iter=4)
+    rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    with _env("SPTB_SIRT_UNFUSED", "1"):
+        rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    assert [r.iterations_run for r in rep] == [r.iterations_run for r in rep2]
+    assert rel(np.asarray(rec.cpu() if hasattr(rec, "cpu") else rec),
+               np.asarray(rec2.cpu() if hasattr(rec2, "cpu") else rec2)) < 1e-4
