@@ -567,6 +567,7 @@ k_fft2_col_pers(const __grid_constant__ CUtensorMap tmap, int strips, int nstrip
         if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
     }
     __syncthreads();
+    const StageTwiddles<LOGN, INV> stw(tw, threadIdx.x / CW2);
     int k = 0;
     for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
         float2* fbuf = base + (k % COLP_BUFS) * BUF;
@@ -581,7 +582,7 @@ k_fft2_col_pers(const __grid_constant__ CUtensorMap tmap, int strips, int nstrip
         for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
         __syncthreads();
         dft16<INV>(v);
-        fft16_stages<LOGN, INV>(v, fbuf + c * LD, j, tw);
+        fft16_stages_pre<LOGN, INV>(v, fbuf + c * LD, j, stw);
         __syncthreads();
 #pragma unroll
         for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
@@ -767,6 +768,7 @@ k_fft1_fwd_pers(const __grid_constant__ CUtensorMap tmap, const float* __restric
         if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
     }
     __syncthreads();
+    const StageTwiddles<LOGN, false> stw(tw, threadIdx.x / CW2);
     int k = 0;
     for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
         float2* fbuf = base + (k % COLP_BUFS) * BUF;
@@ -787,7 +789,7 @@ k_fft1_fwd_pers(const __grid_constant__ CUtensorMap tmap, const float* __restric
         }
         __syncthreads();
         dft16<false>(v);
-        fft16_stages<LOGN, false>(v, fbuf + c * LD, j, tw);
+        fft16_stages_pre<LOGN, false>(v, fbuf + c * LD, j, stw);
         __syncthreads();
 #pragma unroll
         for (int m = 0; m < 16; ++m) fbuf[(j + TP * m) * CW2 + c] = v[(m % NB3) * R3 + m / NB3];
@@ -1051,6 +1053,7 @@ k_fft2_row_unpack_pers(const float2* __restrict__ g, long long M, int Y, const f
     __syncthreads();
     if (dxy) fbar_wait(fb, 0);
     const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const StageTwiddles<LOGN, true> stw(tw, threadIdx.x % (N / 16));
     int k = 0;
     for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
         float2* fbuf = base + (k % COLP_BUFS) * BUF;
@@ -1066,7 +1069,7 @@ k_fft2_row_unpack_pers(const float2* __restrict__ g, long long M, int Y, const f
         for (int r = 0; r < 16; ++r) v[r] = fbuf[rb * N + j + TP * r];
         __syncthreads();
         dft16<true>(v);
-        fft16_stages<LOGN, true>(v, fbuf + rb * N, j, tw);
+        fft16_stages_pre<LOGN, true>(v, fbuf + rb * N, j, stw);
         __syncthreads();
         float* sa = reinterpret_cast<float*>(fbuf);
         float* sbm = sa + RB2 * N;
@@ -1129,6 +1132,7 @@ k_fft1_inv_pers(const __grid_constant__ CUtensorMap tmap, int T, int ngrp, float
     }
     __syncthreads();
     const long long plane = (long long)T * N;
+    const StageTwiddles<LOGN, true> stw(tw, threadIdx.x / CW2);
     int k = 0;
     for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
         float2* fbuf = base + (k % COLP_BUFS) * BUF;
@@ -1143,7 +1147,7 @@ k_fft1_inv_pers(const __grid_constant__ CUtensorMap tmap, int T, int ngrp, float
         for (int r = 0; r < 16; ++r) v[r] = fbuf[(j + TP * r) * CW2 + c];
         __syncthreads();
         dft16<true>(v);
-        fft16_stages<LOGN, true>(v, fbuf + c * LD, j, tw);
+        fft16_stages_pre<LOGN, true>(v, fbuf + c * LD, j, stw);
         __syncthreads();
         float* stg = reinterpret_cast<float*>(fbuf);
 #pragma unroll

@@ -178,5 +178,51 @@ __device__ __forceinline__ void fft16_stages(float2* v, float2* buf, int j, cons
 }
 
 
+
+// The twiddles of stages 2 and 3 depend only on the lane (j), not on the
+// transform: persistent kernels compute them once and keep them in registers
+// (15 + NB3 (R3 - 1) complex values) instead of two table loads and ~30
+// complex products per transform.
+template <int LOGN, bool INV>
+struct StageTwiddles {
+    static constexpr int N = 1 << LOGN, T = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    float2 w2[16];
+    float2 w3[NB3][R3];
+    __device__ __forceinline__ StageTwiddles(const float2* __restrict__ tw, int j) {
+        twiddle_powers<16, INV>(w2, tw, (j & 15) * (N / 256));
+#pragma unroll
+        for (int c = 0; c < NB3; ++c) twiddle_powers<R3, INV>(w3[c], tw, (j + c * T) & 255);
+    }
+};
+
+// fft16_stages with precomputed twiddles (same arithmetic, same results)
+template <int LOGN, bool INV>
+__device__ __forceinline__ void fft16_stages_pre(float2* v, float2* buf, int j, const StageTwiddles<LOGN, INV>& tw) {
+    constexpr int N = 1 << LOGN, T = N / 16, R3 = N / 256, NB3 = 16 / R3;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4(16 * j + r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const float2 x = buf[swz4(j + T * r)];
+        v[r] = r ? cmul(x, tw.w2[r]) : x;
+    }
+    dft16<INV>(v);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4((j >> 4) * 256 + (j & 15) + 16 * r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NB3; ++c) {
+        const int jj = j + c * T;
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const float2 x = buf[swz4(jj + (N / R3) * r)];
+            v[c * R3 + r] = r ? cmul(x, tw.w3[c][r]) : x;
+        }
+        dft_r<R3, INV>(v + c * R3);
+    }
+}
+
 }  // namespace fftcore
 }  // namespace sptb
