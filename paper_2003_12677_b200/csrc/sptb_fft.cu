@@ -1173,6 +1173,88 @@ k_fft1_inv_pers(const __grid_constant__ CUtensorMap tmap, int T, int ngrp, float
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// Persistent version of k_fft2_row_pack_b (radon): strips of 4 rows over
+// all B planes, triple-buffered, stage twiddles in registers.  Planes >= nb
+// load nothing (zeros) but still complete their buffer's mbarrier phase.
+template <int LOGN>
+__global__ void __launch_bounds__(RB2 * (1 << LOGN) / 16, 1)
+k_fft2_row_pack_pers(const float* __restrict__ in, long long M, int Y, const float* __restrict__ dxy, long long n,
+                     long long u0, int nb, float2* __restrict__ g, int nstrip, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, BUF = RB2 * N;
+    extern __shared__ __align__(128) unsigned char rowpbuf_raw[];
+    float2* base = reinterpret_cast<float2*>(rowpbuf_raw);
+    float* fxs = reinterpret_cast<float*>(base + COLP_BUFS * BUF);
+    __shared__ __align__(8) unsigned long long bar[COLP_BUFS + 1];
+    auto load = [&](int s, int k) {
+        const long long gr0 = (long long)s * RB2;
+        const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]);
+        if (b >= nb) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sb) : "memory");
+            return;
+        }
+        const long long u = u0 + b;
+        const bool hb = 2 * u + 1 < n;
+        float* sa = reinterpret_cast<float*>(base + (k % COLP_BUFS) * BUF);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb),
+                     "r"(RB2 * N * 4u * (hb ? 2u : 1u)) : "memory");
+        bulk_g2s(sa, in + (size_t)(2 * u) * M + (size_t)y0 * N, RB2 * N * 4u, sb);
+        if (hb) bulk_g2s(sa + RB2 * N, in + (size_t)(2 * u + 1) * M + (size_t)y0 * N, RB2 * N * 4u, sb);
+    };
+    const unsigned fb = (unsigned)__cvta_generic_to_shared(&bar[COLP_BUFS]);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i <= COLP_BUFS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if (dxy) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(N * 4u) : "memory");
+            bulk_g2s(fxs, dxy, N * 4u, fb);
+        }
+        if ((int)blockIdx.x < nstrip) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    if (dxy) fbar_wait(fb, 0);
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const StageTwiddles<LOGN, false> stw(tw, j);
+    int k = 0;
+    for (int s = blockIdx.x; s < nstrip; s += gridDim.x, ++k) {
+        float2* fbuf = base + (k % COLP_BUFS) * BUF;
+        const long long gr0 = (long long)s * RB2;
+        const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y);
+        if (threadIdx.x == 0 && s + (int)gridDim.x < nstrip) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            load(s + gridDim.x, k + 1);
+        }
+        fbar_wait((unsigned)__cvta_generic_to_shared(&bar[k % COLP_BUFS]), (unsigned)((k / COLP_BUFS) & 1));
+        const bool ha = b < nb, hb = ha && 2 * (u0 + b) + 1 < n;
+        const float* sa = reinterpret_cast<const float*>(fbuf);
+        const float* sbm = sa + RB2 * N;
+        const Deapo dp(dxy, fxs, N, Y, y0 + rb, 1.f);
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int x = j + TP * r;
+            const float d = dp(x);
+            v[r] = make_float2(ha ? sa[rb * N + x] * d : 0.f, hb ? sbm[rb * N + x] * d : 0.f);
+        }
+        __syncthreads();
+        dft16<false>(v);
+        fft16_stages_pre<LOGN, false>(v, fbuf + rb * N, j, stw);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NB3; ++q)
+#pragma unroll
+            for (int r = 0; r < R3; ++r) fbuf[rb * N + j + TP * q + 256 * r] = v[q * R3 + r];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_s2g(g + (size_t)b * M + (size_t)y0 * N, fbuf, RB2 * N * 8u);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 int log2_fft(long long n) {
     if (n < 512 || n > 4096 || (n & (n - 1))) return 0;
     int l = 0;
@@ -1334,7 +1416,15 @@ int row_pack_launch(sptb_plan* p, const float* in, const float* plane, int64_t n
     if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
     constexpr int NT = RB2 * (1 << LOGN) / 16;
     if (row_bulk_ok(in, g)) {
-        // (a persistent triple-buffered version measured 0.477 vs 0.467 ms: not used)
+        const int smp = (int)((COLP_BUFS * 8 * RB2 + 4) * (1 << LOGN));
+        if (smp <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+            const int nstrip = (int)((long long)B * p->Y / RB2);
+            SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
+            k_fft2_row_pack_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
+                in, p->M, p->Y, plane ? p->deapo_xy : nullptr, n, u0, nb, g, nstrip, tw);
+            SPTB_LAUNCHED();
+            return SPTB_OK;
+        }
         const int smb = (int)((8 * RB2 + 4) * (1 << LOGN));
         SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack_b<LOGN>, smb, SPTB_FFT_CARVEOUT));
         k_fft2_row_pack_b<LOGN><<<(unsigned)((long long)B * p->Y / RB2), NT, smb, st>>>(

@@ -15,7 +15,7 @@ def unit_scale(name, val, unit):
     elif unit == "nsecond": v *= 1e-3
     return v  # bytes, or microseconds for durations
 out, traffic = [], {}
-for k in ["k_spmm", "k_sh_tma", "k_fft1_fwd_pers", "k_fft1_inv_pers", "k_fft2_col_pers", "k_fft2_row_unpack_pers", "k_fft2_row_pack_b"]:
+for k in ["k_spmm", "k_sh_tma", "k_fft1_fwd_pers", "k_fft1_inv_pers", "k_fft2_col_pers", "k_fft2_row_unpack_pers", "k_fft2_row_pack_pers"]:
     rep = f"{O}/full_{k}.ncu-rep"
     if not os.path.exists(rep): continue
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
