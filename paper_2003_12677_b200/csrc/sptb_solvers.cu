@@ -110,6 +110,20 @@ struct GridIdx {
     int X, Y;
 };
 
+// elements per thread per k_grid round: 4, or Op::kUnroll for register-heavy
+// fp64 stencil ops (TV: 124-136 registers at 4 left one 256-thread CTA per SM)
+template <class Op, class = void>
+struct OpUnroll {
+    static constexpr int value = 4;
+};
+template <class Op>
+struct OpUnroll<Op, std::void_t<decltype(Op::kUnroll)>> {
+    static constexpr int value = Op::kUnroll;
+};
+
+#ifndef TV_UNROLL
+#define TV_UNROLL 2
+#endif
 template <int K, bool MAX, class Op>
 __global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
     const int b = blockIdx.y;
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
 #pragma unroll
     for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0;
     if (op.enabled(b)) {
-        constexpr int U = 4;
+        constexpr int U = OpUnroll<Op>::value;
         using In = typename Op::In;
         const long long stride = (long long)gridDim.x * RT * U;
         for (long long m0 = blockIdx.x * (long long)RT * U + threadIdx.x; m0 < M; m0 += stride) {
@@ -517,6 +531,7 @@ struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-fi
 
 // rho = (d - b) - grad u  (the stacked target minus fwd(u), unscaled; solvers.py:410-411,438)
 struct OpTvRho {
+    static constexpr int kUnroll = TV_UNROLL;
     const D2 *u, *dx, *dy, *bx, *by;
     D2 *rx, *ry;
     int X, Y;
@@ -535,6 +550,7 @@ struct OpTvRho {
 // MODE 0: p = s, W = deapo p, acc <s,s>;  1: acc <s,s>;  2: p = s + beta p, W = deapo p
 template <typename R, int MODE>
 struct OpTvS {
+    static constexpr int kUnroll = TV_UNROLL;
     using C = typename CT<R>::T;
     C* w;
     D2* p;
@@ -594,6 +610,7 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
 };
 
 struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
+    static constexpr int kUnroll = TV_UNROLL;
     D2 *u, *rx, *ry;
     const D2* p;
     const Unit* us;
@@ -621,6 +638,7 @@ struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
 // isotropic shrink + Bregman update (solvers.py:418-421, 330-341); W = deapo u
 template <typename R>
 struct OpTvShrink {
+    static constexpr int kUnroll = TV_UNROLL;
     using C = typename CT<R>::T;
     const D2* u;
     D2 *dx, *dy, *bx, *by;
