@@ -52,6 +52,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solvers", action="store_true", help="skip the CGLS / TV rates")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle self-check")
     return ap.parse_args()
 
 
@@ -125,13 +126,61 @@ def _oracle_pair(args):
 
 
 def _oracle_setup(n_p, n_theta):
-    from oracle import OGeom, build_oracle_ops, shepp_logan
+    if _ORACLE.get("key") == (n_p, n_theta):
+        return _ORACLE["setup_s"]
+    from oracle import OGeom, build_oracle_ops, parity, shepp_logan
     t0 = time.perf_counter()
     ops = build_oracle_ops(OGeom(n_p, n_theta), kind="ramlak")
     ph = shepp_logan(n_p, 2)
     sino = [ops.radon(x) for x in ph]
-    _ORACLE.update(ops=ops, sino=sino)
-    return time.perf_counter() - t0
+    parity.register("ramlak", ops)
+    _ORACLE.update(ops=ops, sino=sino, key=(n_p, n_theta), setup_s=time.perf_counter() - t0)
+    return _ORACLE["setup_s"]
+
+
+PARITY_SLICES = (0, 1, 31, 62, 63)
+
+
+def parity_check(a, ops, sino, out):
+    """Self-check of the timed production path against the oracle (the
+    reference algorithm, operators.py:153-187), outside the timed region:
+    gridrec of the bench's own sinograms (``out`` = the last timed step) and
+    radon of distinct per-slice images through the same batched plan, on
+    slices {0, 1, 31, 62, 63} (complex pairs 0, 15, 31)."""
+    import numpy as np
+    import torch
+    from oracle import parity
+    from oracle import shepp_logan
+    _oracle_setup(a.n_p, a.n_theta)
+    n = sino.shape[0]
+    check = [z for z in PARITY_SLICES if z < n]
+    pairs = sorted({z // 2 for z in check if 2 * (z // 2) + 1 < n})
+    dev = sino.device
+    g = torch.Generator(device=dev).manual_seed(5)
+    ph = torch.tensor(shepp_logan(a.n_p, 2), dtype=torch.float32, device=dev)
+    img = (ph[torch.arange(n, device=dev) % 2]
+           * torch.linspace(1.0, 0.8, n, device=dev)[:, None, None])
+    img = (img + 0.02 * torch.randn(img.shape, device=dev, generator=g)).contiguous()
+    sin2 = ops.radon(img)
+    torch.cuda.synchronize()
+    sh = {z: sino[z].double().cpu().numpy() for z in {2 * k + j for k in pairs for j in (0, 1)}}
+    rh = {z: out[z].double().cpu().numpy() for z in check}
+    ih = {z: img[z].double().cpu().numpy() for z in sh}
+    s2 = {z: sin2[z].double().cpu().numpy() for z in check}
+    jobs = [("iradon", "ramlak", sh[2 * k] + 1j * sh[2 * k + 1], {}) for k in pairs]
+    jobs += [("radon", "ramlak", ih[2 * k] + 1j * ih[2 * k + 1], {}) for k in pairs]
+    res = parity.run(jobs)
+    gr, ra = {}, {}
+    for i, k in enumerate(pairs):
+        for j, part in ((0, "real"), (1, "imag")):
+            z = 2 * k + j
+            if z in check:
+                gr[z] = parity.rel_l2(rh[z], getattr(res[i], part))
+                ra[z] = parity.rel_l2(s2[z], getattr(res[len(pairs) + i], part))
+    return {"gridrec_rel_l2": max(gr.values()), "radon_rel_l2": max(ra.values()),
+            "slices": check, "tolerance": 1e-4,
+            "ok": max(gr.values()) < 1e-4 and max(ra.values()) < 1e-4,
+            "oracle": "oracle/ restatement of operators.py:153-187 (pinned by tests/golden)"}
 
 
 def cpu_gridrec(n_p, n_theta, passes, pairs_per_core=1, cores=None, warm=0):
@@ -306,6 +355,10 @@ def run_ours(a):
                "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
                "path": "sptb_iradon(plan, pinned host sinograms -> pinned host tomograms)"}
 
+    par = None
+    if rank == 0 and not a.no_parity:
+        par = parity_check(a, ops, sino, out)
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         times, slices, cores, setup = cpu_gridrec(a.n_p, a.n_theta, passes=2, pairs_per_core=1)
@@ -324,7 +377,7 @@ def run_ours(a):
             "config": _config(a), "clocks": clk.summary(), "e2e": e2e,
             "gpu_launches": int(launches), "cufft_execs": int(ffts),
             "roofline": roofline, "roofline_S_H": roofline_sh, "cpu_baseline": cpu,
-            "sirt_iter": sirt, **other, "spmm": spmm, "build_operators_s": build_s,
+            "parity": par, "sirt_iter": sirt, **other, "spmm": spmm, "build_operators_s": build_s,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

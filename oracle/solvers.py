@@ -163,17 +163,62 @@ def _cgls(fwd, adj, norms, b, u, iters, tol, rep):
     return u
 
 
-def o_cgls(sino, ops, max_iter, tol=0.0, nonneg=False):
-    """CGLS on min ||sqrt(w) F (A u - b)|| (solvers.py:230-259; cgs_mode not
-    restated)."""
+def _cgs(sino, ops, iters, tol, rep):
+    """Conjugate gradient squared on the normal equations A^H W A u = A^H W b
+    (solvers.py:262-305): shadow residual fixed at c = A^H W b, per-channel
+    rho / sigma, one residual b - A u per iteration for the report."""
+    w = ops.spectral_weights
+
+    def normal(v):
+        return ops.radon_adjoint(ops.apply_weights(ops.radon(v)))
+
+    c = ops.radon_adjoint(ops.apply_weights(sino))
+    u = np.zeros_like(c)
+    r, shadow, p, q = c.copy(), c.copy(), c.copy(), c.copy()
+    rho = cdot(shadow, r)
+    bn = wnorms(sino, w)
+    for _ in range(iters):
+        v = normal(p)
+        sig = cdot(shadow, v)
+        live = np.abs(sig) > 0
+        if not live.any():
+            break
+        al = np.where(live, sdiv(rho, sig, np.zeros_like(rho)), 0.0)
+        h = q - cscale(al, v)
+        stp = q + h
+        u = u + cscale(al, stp)
+        r = r - cscale(al, normal(stp))
+        rc = wnorms(sino - ops.radon(u), w)
+        rep.history.append(rss(rc))
+        rep.iterations += 1
+        _finite(u, "cgs")
+        if np.max(sdiv(rc, bn, np.zeros_like(rc))) <= tol:
+            rep.converged = True
+            break
+        rn = cdot(shadow, r)
+        if not (np.abs(rn) > 0).any():
+            break
+        be = sdiv(rn, rho, np.zeros_like(rn))
+        rho = rn
+        q = r + cscale(be, h)
+        p = q + cscale(be, h + cscale(be, p))
+    return u
+
+
+def o_cgls(sino, ops, max_iter, tol=0.0, nonneg=False, cgs_mode=False):
+    """CGLS on min ||sqrt(w) F (A u - b)|| (solvers.py:230-259); ``cgs_mode``
+    runs the CGS recurrence on the normal equations instead (:247-248)."""
     w = ops.spectral_weights
     u = np.zeros(ops.g.grid, dtype=complex if np.iscomplexobj(sino) else float)
     rep = OReport()
     if rss(wnorms(sino, w)) == 0.0:
         rep.converged = True
         return u, rep
-    u = _cgls(ops.radon, lambda r: ops.radon_adjoint(ops.apply_weights(r)),
-              lambda r: wnorms(r, w), sino, u, max_iter, tol, rep)
+    if cgs_mode:
+        u = _cgs(sino, ops, max_iter, tol, rep)
+    else:
+        u = _cgls(ops.radon, lambda r: ops.radon_adjoint(ops.apply_weights(r)),
+                  lambda r: wnorms(r, w), sino, u, max_iter, tol, rep)
     if nonneg:
         u = _nonneg(u)
     return u, rep

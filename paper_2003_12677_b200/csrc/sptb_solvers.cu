@@ -527,6 +527,134 @@ struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-fi
     }
 };
 
+// ------------------------------------------------------------------ grid ops (CGS, fp64 vectors)
+// Conjugate gradient squared on A^H W A u = A^H W b (solvers.py:262-305):
+// r, shadow, p, q, h, v are grid vectors; "step" = q + h is never stored.
+
+template <typename R>
+struct OpCgsInit {  // c = deapo*y*scale ; r = shadow = p = q = c ; rho = <c,c> ; W = deapo p
+    using C = typename CT<R>::T;
+    C* w;
+    D2 *r, *sh, *p, *q;
+    const R* deapo;
+    double scale;
+    struct In { C y; R d; };
+    __device__ bool enabled(int) const { return true; }
+    __device__ In load(int, size_t i, long long m) const { return In{w[i], deapo[m]}; }
+    __device__ void apply(int, size_t i, long long, const In& v, double (&acc)[2]) const {
+        const double d = (double)v.d;
+        const D2 c = make_double2(v.y.x * d * scale, v.y.y * d * scale);
+        acc[0] += c.x * c.x;
+        acc[1] += c.y * c.y;
+        r[i] = c;
+        sh[i] = c;
+        p[i] = c;
+        q[i] = c;
+        w[i] = rc<R>(c.x * d, c.y * d);
+    }
+};
+
+template <typename R>
+struct OpCgsV {  // v = deapo*y*scale (= M p) ; sigma = <shadow, v>
+    using C = typename CT<R>::T;
+    const C* w;
+    const D2* sh;
+    D2* v;
+    const R* deapo;
+    double scale;
+    struct In { C y; D2 s; R d; };
+    __device__ bool enabled(int) const { return true; }
+    __device__ In load(int, size_t i, long long m) const { return In{w[i], sh[i], deapo[m]}; }
+    __device__ void apply(int, size_t i, long long, const In& x, double (&acc)[2]) const {
+        const double d = (double)x.d * scale;
+        const D2 vv = make_double2(x.y.x * d, x.y.y * d);
+        acc[0] += x.s.x * vv.x;
+        acc[1] += x.s.y * vv.y;
+        v[i] = vv;
+    }
+};
+
+template <typename R>
+struct OpCgsStep {  // h = q - alpha v ; u += alpha (q + h) ; W = deapo (q + h) ; non-finite u
+    using C = typename CT<R>::T;
+    D2 *u, *h;
+    const D2 *q, *v;
+    C* w;
+    const R* deapo;
+    const Unit* us;
+    struct In { D2 x, qq, vv; R d; };
+    __device__ bool enabled(int) const { return true; }
+    __device__ In load(int, size_t i, long long m) const { return In{u[i], q[i], v[i], deapo[m]}; }
+    __device__ void apply(int b, size_t i, long long, const In& e, double (&acc)[1]) const {
+        const Unit& un = us[b];
+        const double d = (double)e.d;
+        D2 x = e.x, st = make_double2(0, 0);
+        if (un.stepped) {
+            const D2 hh = make_double2(e.qq.x - un.alpha[0] * e.vv.x, e.qq.y - un.alpha[1] * e.vv.y);
+            st = make_double2(e.qq.x + hh.x, e.qq.y + hh.y);
+            x.x += un.alpha[0] * st.x;
+            x.y += un.alpha[1] * st.y;
+            h[i] = hh;
+            u[i] = x;
+        }
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+        w[i] = rc<R>(st.x * d, st.y * d);
+    }
+};
+
+template <typename R>
+struct OpCgsResid {  // r -= alpha deapo*y*scale (= M step) ; rho_new = <shadow, r> ; W = deapo u
+    using C = typename CT<R>::T;
+    C* w;
+    D2* r;
+    const D2 *sh, *u;
+    const R* deapo;
+    double scale;
+    const Unit* us;
+    struct In { C y; D2 rr, s, x; R d; };
+    __device__ bool enabled(int) const { return true; }
+    __device__ In load(int, size_t i, long long m) const { return In{w[i], r[i], sh[i], u[i], deapo[m]}; }
+    __device__ void apply(int b, size_t i, long long, const In& e, double (&acc)[2]) const {
+        const Unit& un = us[b];
+        const double d = (double)e.d;
+        D2 rr = e.rr;
+        if (un.stepped) {
+            rr.x -= un.alpha[0] * (e.y.x * d * scale);
+            rr.y -= un.alpha[1] * (e.y.y * d * scale);
+            r[i] = rr;
+        }
+        acc[0] += e.s.x * rr.x;
+        acc[1] += e.s.y * rr.y;
+        w[i] = rc<R>(e.x.x * d, e.x.y * d);
+    }
+};
+
+template <typename R>
+struct OpCgsDir {  // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
+    using C = typename CT<R>::T;
+    const D2 *r, *h;
+    D2 *q, *p;
+    C* w;
+    const R* deapo;
+    const Unit* us;
+    struct In { D2 rr, hh, pp; R d; };
+    __device__ bool enabled(int) const { return true; }
+    __device__ In load(int, size_t i, long long m) const { return In{r[i], h[i], p[i], deapo[m]}; }
+    __device__ void apply(int b, size_t i, long long, const In& e, double (&)[1]) const {
+        const Unit& un = us[b];
+        D2 pp = e.pp;
+        if (un.active) {
+            const double b0 = un.beta[0], b1 = un.beta[1];
+            const D2 qq = make_double2(e.rr.x + b0 * e.hh.x, e.rr.y + b1 * e.hh.y);
+            pp = make_double2(qq.x + b0 * (e.hh.x + b0 * pp.x), qq.y + b1 * (e.hh.y + b1 * pp.y));
+            q[i] = qq;
+            p[i] = pp;
+        }
+        const double d = (double)e.d;
+        w[i] = rc<R>(pp.x * d, pp.y * d);
+    }
+};
+
 // ------------------------------------------------------------------ grid ops (TV)
 
 // rho = (d - b) - grad u  (the stacked target minus fwd(u), unscaled; solvers.py:410-411,438)
@@ -976,6 +1104,57 @@ __global__ void k_cgls_beta(Unit* us, const double* ss, int B, int tv) {
     (void)tv;
 }
 
+// CGS (solvers.py:280-291): sigma = <shadow, M p>; any channel |sigma| > 0
+// steps with alpha = rho / sigma (safe division), else the unit stops
+// (breakdown: converged = False, not thrown)
+__global__ void k_cgs_alpha(Unit* us, const double* sig, int B) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    un.stepped = 0;
+    un.alpha[0] = un.alpha[1] = 0.0;
+    if (!un.active) return;
+    bool any = false;
+    for (int c = 0; c < 2; ++c) {
+        const bool a = !(un.single && c == 1) && fabs(sig[2 * b + c]) > 0;
+        un.act[c] = a;
+        any = any || a;
+    }
+    if (!any) {
+        un.status = ST_STOPPED;
+        un.active = 0;
+        un.converged = 0;
+        return;
+    }
+    for (int c = 0; c < 2; ++c) un.alpha[c] = un.act[c] ? safe_div(un.gamma[c], sig[2 * b + c], 0.0) : 0.0;
+    un.stepped = 1;
+}
+
+// residual of b - A u (history, non-finite u, tol), then rho_new / beta
+// (solvers.py:292-304)
+__global__ void k_cgs_check(Unit* us, const double* ac, const double* nf, const double* rho_new,
+                            int P, int it, int B, double* hist, double tol) {
+    const int b = threadIdx.x;
+    if (b >= B) return;
+    Unit& un = us[b];
+    un.beta[0] = un.beta[1] = 0.0;
+    if (!un.stepped) return;
+    record_residual(un, ac + 2 * b, P, it, B, b, hist, nf[b] > 0, false, tol, false);
+    if (!un.active) return;
+    bool any = false;
+    for (int c = 0; c < 2; ++c) any = any || (!(un.single && c == 1) && fabs(rho_new[2 * b + c]) > 0);
+    if (!any) {
+        un.status = ST_STOPPED;
+        un.active = 0;
+        un.converged = 0;
+        return;
+    }
+    for (int c = 0; c < 2; ++c) {
+        un.beta[c] = (un.single && c == 1) ? 0.0 : safe_div(rho_new[2 * b + c], un.gamma[c], 0.0);
+        un.gamma[c] = rho_new[2 * b + c];
+    }
+}
+
 // non-finite u after a step overrides the tol decision (solvers.py:217 precedes :219)
 __global__ void k_flag_nonfinite(Unit* us, const double* nf, int B, int only_stepped) {
     const int b = threadIdx.x;
@@ -1056,6 +1235,7 @@ struct Solver {
     // float64 Krylov state (CGLS / TV)
     D2 *Ud = nullptr, *Pd = nullptr, *RHd = nullptr;
     D2 *dx = nullptr, *dy = nullptr, *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;
+    D2 *Rg = nullptr, *SHg = nullptr, *Qg = nullptr, *Hg = nullptr, *Vg = nullptr;  // CGS
     double *part = nullptr, *sums = nullptr, *sums2 = nullptr, *sums3 = nullptr, *hist = nullptr;
     Unit* us = nullptr;
     Global* gl = nullptr;
@@ -1095,7 +1275,7 @@ struct Solver {
         for (auto& kv : owned) p->pool.push_back(kv);
     }
 
-    int init(int algo, int max_iter) {
+    int init(int algo, int max_iter, bool cgs) {
         st = p->stream;
         SPTB_TRY(ensure_work(p, B));
         const size_t gb = sizeof(C) * (size_t)B * p->M, sb = sizeof(C) * (size_t)B * p->N;
@@ -1114,6 +1294,9 @@ struct Solver {
         }
         if (algo == SPTB_ALGO_TV) {
             for (D2** q : {&dx, &dy, &bx, &by, &rx, &ry}) SPTB_TRY(alloc((void**)q, gd));
+        }
+        if (algo == SPTB_ALGO_CGLS && cgs) {
+            for (D2** q : {&Rg, &SHg, &Qg, &Hg, &Vg}) SPTB_TRY(alloc((void**)q, gd));
         }
         nblk_grid = std::max(1, 1184 / B);
         nblk_spec = 1184;
@@ -1390,6 +1573,47 @@ struct Solver {
         return SPTB_OK;
     }
 
+    // ---------------------------------------------------------------- CGS
+    // cgs_mode of solve_cgls (solvers.py:262-305).  M v = A^H W A v costs one
+    // forward and one adjoint application; an iteration applies M twice and
+    // A once more for the reported residual b - A u.
+    int normal_apply() {  // W holds deapo*v on entry, IFFT2(S_w F(v)) on exit
+        SPTB_TRY(forward_spec(QH, nullptr));
+        return adjoint_grid(QH, true);
+    }
+
+    int run_cgs(const sptb_solver_config& cfg) {
+        const double invP = 1.0 / p->P;
+        // c = A^H W b ; r = shadow = p = q = c ; rho = <shadow, r>
+        SPTB_TRY(adjoint_grid(BH, true));
+        SPTB_TRY(grid<2>(OpCgsInit<R>{W, Rg, SHg, Pd, Qg, deapo(), invP}, sums2));
+        k_cgls_init<<<1, 64, 0, st>>>(us, sums2, B);  // gamma := rho
+        SPTB_TRY(unit_kernel_done());
+        for (int it = 0; it < cfg.max_iter; ++it) {
+            bool stop;
+            SPTB_TRY(poll(it, &stop));
+            if (stop) break;
+            // v = M p ; sigma ; alpha
+            SPTB_TRY(normal_apply());
+            SPTB_TRY(grid<2>(OpCgsV<R>{W, SHg, Vg, deapo(), invP}, sums2));
+            k_cgs_alpha<<<1, 64, 0, st>>>(us, sums2, B);
+            SPTB_TRY(unit_kernel_done());
+            // h = q - alpha v ; u += alpha (q + h) ; r -= alpha M (q + h)
+            SPTB_TRY(grid<1>(OpCgsStep<R>{Ud, Hg, Qg, Vg, W, deapo(), us}, sums3));
+            SPTB_TRY(normal_apply());
+            SPTB_TRY(grid<2>(OpCgsResid<R>{W, Rg, SHg, Ud, deapo(), invP, us}, sums2));
+            // reported residual b - A u ; tol ; rho_new ; beta
+            SPTB_TRY(forward_spec(RH, BH));
+            SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
+            k_cgs_check<<<1, 64, 0, st>>>(us, sums, sums3, sums2, p->P, it, B, hist, cfg.tol);
+            SPTB_TRY(unit_kernel_done());
+            // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
+            SPTB_TRY(grid<0>(OpCgsDir<R>{Rg, Hg, Qg, Pd, W, deapo(), us}, nullptr));
+        }
+        if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
+        return SPTB_OK;
+    }
+
     // ---------------------------------------------------------------- TV
     int run_tv(const sptb_solver_config& cfg) {
         const double invP = 1.0 / p->P;
@@ -1478,7 +1702,7 @@ int solve_typed(sptb_plan* p, const sptb_solver_config& cfg, const void* sino, i
     Solver<R> sv;
     sv.p = p;
     sv.B = Bmax;
-    SPTB_TRY(sv.init(cfg.algorithm, iters_cap));
+    SPTB_TRY(sv.init(cfg.algorithm, iters_cap, cfg.cgs_mode != 0));
     std::vector<double> hbuf((size_t)iters_cap * Bmax);
     std::vector<Unit> ubuf(Bmax);
     for (int64_t u0 = 0; u0 < units; u0 += Bmax) {
@@ -1498,7 +1722,9 @@ int solve_typed(sptb_plan* p, const sptb_solver_config& cfg, const void* sino, i
         switch (cfg.algorithm) {
             case SPTB_ALGO_FBP: SPTB_TRY(sv.run_fbp()); break;
             case SPTB_ALGO_SIRT: SPTB_TRY(sv.run_sirt(cfg)); break;
-            case SPTB_ALGO_CGLS: SPTB_TRY(sv.run_cgls(cfg)); break;
+            case SPTB_ALGO_CGLS:
+                SPTB_TRY(cfg.cgs_mode ? sv.run_cgs(cfg) : sv.run_cgls(cfg));
+                break;
             case SPTB_ALGO_TV: SPTB_TRY(sv.run_tv(cfg)); break;
             default: return fail(SPTB_ERR_ARG, "unknown algorithm");
         }

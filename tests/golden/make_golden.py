@@ -134,6 +134,37 @@ def solvers_case(sp):
     return out
 
 
+def cgs_case(sp):
+    """cgs_mode=True runs of solve_cgls (solvers.py:247-248,262-305) on the
+    solvers_case setup: paired and single, filter none and hamming, nonneg, tol."""
+    geom = sp.ScanGeometry(n_p=32, n_theta=20)
+    yy, xx = np.mgrid[0:32, 0:32]
+    a = np.clip(14 - np.hypot(xx - 16, yy - 16), 0, 1) * 0.8
+    b = (np.hypot(xx - 12, yy - 18) < 6).astype(float)
+    rng = np.random.default_rng(7)
+    out = {}
+    for kind in ("none", "hamming"):
+        ops = sp.build_operators(geom, filter_kind=kind)
+        sa = ops.radon(a)
+        sb = ops.radon(b) + 0.01 * rng.standard_normal(geom.sino_shape)
+        out[f"{kind}_sino_a"] = sa
+        out[f"{kind}_sino_b"] = sb
+        for tag, cfg in (("", sp.SolverConfig(algorithm="cgls", max_iter=8, cgs_mode=True, filter=kind)),
+                         ("_nonneg", sp.SolverConfig(algorithm="cgls", max_iter=6, cgs_mode=True,
+                                                     nonneg=True, filter=kind)),
+                         ("_tol", sp.SolverConfig(algorithm="cgls", max_iter=40, cgs_mode=True,
+                                                  tol=0.02, filter=kind))):
+            rp, rep_p = sp.solve(sp.pair_complex(sa, sb), ops, cfg)
+            ra, rep_a = sp.solve(sa, ops, cfg)
+            out[f"{kind}{tag}_rec_pair"] = rp
+            out[f"{kind}{tag}_rec_a"] = ra
+            out[f"{kind}{tag}_hist_pair"] = np.asarray(rep_p.residual_history)
+            out[f"{kind}{tag}_hist_a"] = np.asarray(rep_a.residual_history)
+            out[f"{kind}{tag}_conv_pair"] = rep_p.converged
+            out[f"{kind}{tag}_conv_a"] = rep_a.converged
+    return out
+
+
 def pipeline_case(sp):
     """run_pipeline on an odd 5-slice stack (test_pipeline.py:131-136)."""
     geom = sp.ScanGeometry(n_p=32, n_theta=12, n_z=5)
@@ -183,6 +214,10 @@ def main():
             np.savez_compressed(os.path.join(OUT, f"density_{name}.npz"), **density_case(sp, name, gkw, kkw))
             print("wrote density", name)
     if "--density-only" in sys.argv:
+        return
+    np.savez_compressed(os.path.join(OUT, "solvers_cgs_g32.npz"), **cgs_case(sp))
+    print("wrote cgs")
+    if "--cgs-only" in sys.argv:
         return
     for name, gkw, kkw in GEOMS:
         d = operators_case(sp, name, gkw, kkw)

@@ -73,6 +73,57 @@ def test_solver_matches_reference(sb, sol, algo, iters, prec):
     np.testing.assert_allclose(rep_a.residual_history, hist_a, rtol=tol)
 
 
+CGS_TAGS = [("", dict(max_iter=8)), ("_nonneg", dict(max_iter=6, nonneg=True)),
+            ("_tol", dict(max_iter=40, tol=0.02))]
+
+
+@pytest.mark.parametrize("prec", ["complex64", "complex128"])
+@pytest.mark.parametrize("kind", ["none", "hamming"])
+@pytest.mark.parametrize("tag,kw", CGS_TAGS)
+def test_cgs_mode_matches_reference(sb, prec, kind, tag, kw):
+    """solve_cgls(cfg.cgs_mode=True): CGS on the normal equations
+    (solvers.py:247-248,262-305) vs the unmodified reference's output.
+    complex128: 1e-8, or -- where the recurrence is chaotic (filter none: CGS
+    squares the residual polynomial of the cond^2 normal equations) -- 3x the
+    spread of the reference algorithm itself under 1e-15 relative rounding
+    perturbations of its operators (oracle/emulate.py PerturbedOperators,
+    6 seeds; up to 1e-5 for pairs and 8e-3 for single slices).  complex64:
+    CGS, like CGLS, amplifies single-precision operator rounding; the bar is
+    1e-3 or 2x the reference algorithm's own deviation when its operators run
+    in complex64 (oracle/emulate.py)."""
+    d = load_golden("solvers_cgs_g32.npz")
+    ops = _ops(sb, kind, prec)
+    cfg = sb.SolverConfig(algorithm="cgls", cgs_mode=True, filter=kind, **kw)
+    sa, sbb = d[f"{kind}_sino_a"], d[f"{kind}_sino_b"]
+    for sino, key in ((sa + 1j * sbb, "pair"), (sa, "a")):
+        ref, hist = d[f"{kind}{tag}_rec_{key}"], d[f"{kind}{tag}_hist_{key}"]
+        rec, rep = sb.solve(sino, ops, cfg)
+        assert np.iscomplexobj(rec) == (key == "pair")
+        if prec == "complex128":
+            from oracle import OGeom, build_oracle_ops, o_solve
+            from oracle.emulate import PerturbedOperators
+            oops = build_oracle_ops(OGeom(32, 20), kind=kind)
+            runs = [o_solve(sino, PerturbedOperators(oops, 1e-15, seed), "cgls", cgs_mode=True, **kw)
+                    for seed in range(6)]
+            tol_r = max(TOL[prec], 3.0 * max(rel(r, ref) for r, _ in runs))
+            tol_h = max(TOL[prec], 3.0 * max(float(np.max(np.abs(np.asarray(e.history) - hist) / hist))
+                                             for _, e in runs))
+        else:
+            from oracle import OGeom, build_oracle_ops, o_solve
+            from oracle.emulate import Fp32PipelineOperators
+            emu, erep = o_solve(sino, Fp32PipelineOperators(build_oracle_ops(OGeom(32, 20), kind=kind)),
+                                "cgls", cgs_mode=True, **{k.replace("_enabled", ""): v
+                                                          for k, v in kw.items()})
+            tol_r = max(1e-3, 2.0 * rel(emu, ref))
+            tol_h = max(1e-3, 2.0 * float(np.max(np.abs(np.asarray(erep.history) - hist) / hist)))
+        assert rel(rec, ref) <= tol_r, (key, rel(rec, ref), tol_r)
+        assert rep.iterations_run == len(hist)
+        np.testing.assert_allclose(rep.residual_history, hist, rtol=tol_h)
+        assert rep.converged == bool(d[f"{kind}{tag}_conv_{key}"])
+        if kw.get("nonneg"):
+            assert np.min(np.real(rec)) >= 0.0
+
+
 @pytest.mark.parametrize("prec", ["complex64", "complex128"])
 def test_sirt_variants(sb, sol, prec):
     ops = _ops(sb, "hamming", prec)

@@ -106,6 +106,24 @@ def test_solver_variants(sol):
     assert rel(r, sol["tv_mu_rec"]) <= 1e-10
 
 
+CGS_TAGS = [("", dict(max_iter=8)), ("_nonneg", dict(max_iter=6, nonneg=True)),
+            ("_tol", dict(max_iter=40, tol=0.02))]
+
+
+@pytest.mark.parametrize("kind", ["none", "hamming"])
+@pytest.mark.parametrize("tag,kw", CGS_TAGS)
+def test_cgs_mode_matches_reference(kind, tag, kw):
+    """solve_cgls with cgs_mode=True (solvers.py:247-248,262-305)."""
+    d = load_golden("solvers_cgs_g32.npz")
+    ops = build_oracle_ops(OGeom(n_p=32, n_theta=20), kind=kind)
+    sa, sb = d[f"{kind}_sino_a"], d[f"{kind}_sino_b"]
+    for sino, key in ((sa + 1j * sb, "pair"), (sa, "a")):
+        r, rep = o_solve(sino, ops, "cgls", cgs_mode=True, **kw)
+        assert rel(r, d[f"{kind}{tag}_rec_{key}"]) <= 1e-10
+        np.testing.assert_allclose(rep.history, d[f"{kind}{tag}_hist_{key}"], rtol=1e-10)
+        assert rep.converged == bool(d[f"{kind}{tag}_conv_{key}"])
+
+
 DENSITY_FILES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "density_*.npz")))
 
 
