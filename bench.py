@@ -53,6 +53,9 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solvers", action="store_true", help="skip the CGLS / TV rates")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle self-check")
+    ap.add_argument("--pipeline-slices", type=int, default=512,
+                    help="slices of the strong-scaling SIRT pipeline run (BASELINE configs[2]); 0 = skip")
+    ap.add_argument("--pipeline-iters", type=int, default=100)
     return ap.parse_args()
 
 
@@ -325,6 +328,7 @@ def run_ours(a):
     # ---- SIRT iteration throughput (setup excluded by differencing)
     sirt = _sirt_rate(sb, geom, sino, a, dev, stream)
     other = {} if a.no_solvers else _other_solvers(sb, geom, sino, a, dev, stream)
+    pipe = _pipeline_sirt(sb, a, world, rank, dev) if a.pipeline_slices > 0 else None
 
     # ---- end to end through the C ABI with host buffers (pinned)
     e2e = None
@@ -377,7 +381,7 @@ def run_ours(a):
             "config": _config(a), "clocks": clk.summary(), "e2e": e2e,
             "gpu_launches": int(launches), "cufft_execs": int(ffts),
             "roofline": roofline, "roofline_S_H": roofline_sh, "cpu_baseline": cpu,
-            "parity": par, "sirt_iter": sirt, **other, "spmm": spmm, "build_operators_s": build_s,
+            "parity": par, "sirt_iter": sirt, **other, "pipeline_sirt": pipe, "spmm": spmm, "build_operators_s": build_s,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -447,6 +451,94 @@ def _other_solvers(sb, geom, sino_clean, a, dev, stream):
     return out
 
 
+def _pipeline_sirt(sb, a, world, rank, dev):
+    """BASELINE configs[2] as a strong-scaling run: SIRT (Hamming, BB,
+    ``--pipeline-iters`` iterations) on a ``--pipeline-slices`` stack of
+    2048^2 x 1536 noisy sinograms through run_pipeline, partitioned by slice
+    over the ranks.  The stack and the output volume are memory-mapped files
+    in /dev/shm that every rank maps (as the CLI maps SPTOMO01 volumes): each
+    rank copies its own slices host -> device over its own PCIe link and
+    writes its own reconstructed slices back -- no data-path collective.  The
+    timed region runs from the first H2D to the last D2H (CUDA events,
+    max over ranks)."""
+    import hashlib
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from oracle import shepp_logan  # synthetic phantom only
+
+    nz, iters = a.pipeline_slices, a.pipeline_iters
+    geom = sb.ScanGeometry(n_p=a.n_p, n_theta=a.n_theta, n_z=nz)
+    T, P = geom.sino_shape
+    Y, X = geom.grid_shape
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    tag = os.environ.get("TORCHELASTIC_RUN_ID", "") + os.environ.get("MASTER_PORT", str(os.getpid()))
+    in_path = os.path.join(base, f"sptb_bench_{tag}_sino.f32")
+    out_path = os.path.join(base, f"sptb_bench_{tag}_vol.f32")
+    ops_h = sb.build_operators(sb.ScanGeometry(n_p=a.n_p, n_theta=a.n_theta), filter_kind="hamming",
+                               max_batch=32)
+    if rank == 0:
+        sino = np.memmap(in_path, dtype=np.float32, mode="w+", shape=(nz, T, P))
+        np.memmap(out_path, dtype=np.float32, mode="w+", shape=(nz, Y, X)).flush()
+        ph = torch.tensor(shepp_logan(a.n_p)[0], dtype=torch.float32, device=dev)
+        clean = ops_h.radon(ph[None].expand(2, -1, -1).contiguous())[0]
+        g = torch.Generator(device=dev).manual_seed(3)
+        amp = float(clean.abs().max())
+        for z0 in range(0, nz, 64):
+            k = min(64, nz - z0)
+            sc = torch.linspace(1.0, 0.8, nz, device=dev)[z0:z0 + k]
+            blk = clean[None] * sc[:, None, None]
+            blk = blk + 0.02 * amp * torch.randn(blk.shape, device=dev, generator=g)
+            sino[z0:z0 + k] = blk.cpu().numpy()
+        sino.flush()
+        del sino
+    if world > 1:
+        dist.barrier()
+    stack = sb.SinogramStack(data=np.memmap(in_path, dtype=np.float32, mode="r", shape=(nz, T, P)),
+                             geometry=geom)
+    out = np.memmap(out_path, dtype=np.float32, mode="r+", shape=(nz, Y, X))
+    cfg = sb.SolverConfig(algorithm="sirt", max_iter=iters)
+    # warm-up (plans, solver buffers, page cache) on a short run
+    sb.run_pipeline(stack, sb.SolverConfig(algorithm="sirt", max_iter=2), ops=ops_h, out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, rep = sb.run_pipeline(stack, cfg, ops=ops_h, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    res = None
+    if rank == 0:
+        h = hashlib.sha256()
+        for z in list(range(0, nz, 64)) + [nz - 1]:
+            h.update(np.ascontiguousarray(out[z]).tobytes())
+        res = {"value": nz * iters * 1e3 / ms, "unit": "slice-iterations/s", "n_gpus": world,
+               "ms": ms, "scaling": "strong", "slices": nz, "iterations": iters,
+               "iterations_run": rep.iterations_run, "final_residual_max": max(rep.residual_history),
+               "volume_digest": h.hexdigest()[:16],
+               "h2d_bytes": nz * T * P * 4, "d2h_bytes": nz * Y * X * 4,
+               "workload": f"SIRT-{iters} (hamming, BB) {nz} slices {a.n_p}^2x{a.n_theta}, 2% noise, "
+                           "run_pipeline over all ranks (BASELINE configs[2]); per-rank H2D/D2H of "
+                           "its own slices from/to memory-mapped volumes inside the timed region"}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        for pth in (in_path, out_path):
+            try:
+                os.unlink(pth)
+            except OSError:
+                pass
+    return res
+
+
 def _traffic_from_profiles():
     """dram bytes per launch from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "spmm_traffic.json")
@@ -457,8 +549,23 @@ def _traffic_from_profiles():
         return {}
 
 
+def _relaunch_distributed(a):
+    """``--gpus N`` outside torchrun: re-exec this script as N ranks (one
+    process per GPU, NCCL) the way the driver launches it."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     a = _args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch_distributed(a)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -87,6 +87,11 @@ int sptb_plan_create(sptb_plan** out, const sptb_geometry* geom,
                      int32_t max_batch, int32_t device, double threshold);
 int sptb_plan_destroy(sptb_plan* plan);
 
+/* Re-read the SPTB_* path-selection environment switches (tests and A/B
+ * measurements only; no reference counterpart).  The library reads them once
+ * at first use; production never sets them. */
+int sptb_reload_switches(void);
+
 /* CUDA stream (cudaStream_t as void*) for all subsequent work; NULL = legacy. */
 int sptb_plan_set_stream(sptb_plan* plan, void* stream);
 

@@ -26,18 +26,16 @@ from .pipeline import (PAIRING_TOL, ChunkPlan, SinogramStack, TomogramStack,
 from ._lib import LIB_PATH, launch_count
 from .cache import (CACHE_MAGIC, CACHE_VERSION, MatrixCacheKey, SparseGridCSR, build_matrix,
                     cache_load, cache_store, make_cache_key)
-from .io import (KIND_INTENSITY, KIND_SINOGRAM, KIND_TOMOGRAM, Metrics, VolumeFile,
-                 compute_metrics, normalize, phantom_shepp_logan, read_volume,
-                 simulate_intensity, sinogram_geometry, snr, write_volume)
+from .io import (KIND_INTENSITY, KIND_SINOGRAM, KIND_TOMOGRAM, VolumeFile, VolumeHeader,
+                 VolumeWriter, read_header, read_volume, write_volume)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ALGORITHMS", "CACHE_MAGIC", "CACHE_VERSION", "ChunkPlan", "MatrixCacheKey", "cache_load",
     "cache_store", "make_cache_key", "SparseGridCSR", "build_matrix", "KIND_INTENSITY",
-    "KIND_SINOGRAM", "KIND_TOMOGRAM", "Metrics", "VolumeFile", "compute_metrics", "normalize",
-    "phantom_shepp_logan", "read_volume", "simulate_intensity", "sinogram_geometry", "snr",
-    "write_volume", "deapodization_compute", "kernel_eval", "kernel_transform",
+    "KIND_SINOGRAM", "KIND_TOMOGRAM", "VolumeFile", "VolumeHeader", "VolumeWriter",
+    "read_header", "read_volume", "write_volume", "deapodization_compute", "kernel_eval", "kernel_transform",
     "polar_coords", "stencil_offsets", "SparseCOO", "build_coo", "coo_to_csr", "prune", "CorruptCacheError", "DEFAULT_FILTERS",
     "Deapodization", "density_filter_solve", "DeviceGridCSR", "DivergenceError", "FILTER_KINDS",
     "FileFormatError", "FilterSpec", "GridTooLargeError", "InvalidFlatFieldError",

@@ -24,7 +24,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-I", os.path.join(ROOT, "include")]
 
 SOURCES = ["sptb_plan.cu", "sptb_build.cu", "sptb_kernels.cu", "sptb_spmm_api.cu",
-           "sptb_solvers.cu", "sptb_patch.cu", "sptb_stile.cu", "sptb_fft.cu", "sptb_density.cu"]
+           "sptb_solvers.cu", "sptb_patch.cu", "sptb_spmm_s.cu", "sptb_fft.cu", "sptb_density.cu"]
 
 
 def _newer(src_files, target):

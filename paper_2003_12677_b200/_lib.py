@@ -53,6 +53,7 @@ SIGNATURES = [
     ("sptb_plan_create", C.c_int, [C.POINTER(_P), C.POINTER(Geometry), C.POINTER(Kernel),
                                    C.c_int32, C.c_int32, C.c_int32, C.c_double]),
     ("sptb_plan_destroy", C.c_int, [_P]),
+    ("sptb_reload_switches", C.c_int, []),
     ("sptb_plan_set_stream", C.c_int, [_P, _P]),
     ("sptb_plan_set_filter", C.c_int, [_P, C.POINTER(C.c_double), C.c_int64]),
     ("sptb_plan_calibrate", C.c_int, [_P, C.POINTER(C.c_double)]),

@@ -378,17 +378,13 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         }
     }
     sp.n_reg = sp.slot_mode ? cnt[npatch] : N;
-    std::vector<int> cls_start;  // slot mode: per patch, s' start of each border class (+ end)
 #ifndef SPTB_CLASS_ORDER
 #define SPTB_CLASS_ORDER 1
 #endif
     if (sp.slot_mode && SPTB_CLASS_ORDER) {
         // within a patch: border class (TL, T, TR, R, BR, B, BL, L, interior),
-        // then stencil-centre cell, then sample.  Every neighbour of the patch
-        // then finds the samples it shares with this patch (an edge column/row
-        // or a corner) in at most two contiguous s' runs, and the samples of
-        // one centre cell are contiguous (sptb_stile.cu stages runs by bulk copy)
-        cls_start.assign((size_t)npatch * STILE_NCLS1, 0);
+        // then stencil-centre cell, then sample: each neighbour of the patch
+        // finds the samples it shares with it in at most two contiguous runs
         std::vector<std::pair<uint64_t, int>> key;
         for (int64_t q = 0; q < npatch; ++q) {
             key.clear();
@@ -396,23 +392,16 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
             for (int64_t r = cnt[q]; r < cnt[q + 1]; ++r) {
                 const int sm = order[r];
                 const int lx = cx[sm] - PATCH_W * px - 1, ly = cy[sm] - PATCH_W * py;
-                const int c = stile_class(lx, ly);
+                const int c = border_class(lx, ly);
                 key.push_back({((uint64_t)c << 40) | ((uint64_t)(ly * PATCH_W + lx) << 32) | (uint64_t)sm, sm});
             }
             std::sort(key.begin(), key.end());
             int64_t r = cnt[q];
-            for (int c = 0; c < STILE_NCLS1; ++c) cls_start[q * STILE_NCLS1 + c] = (int)cnt[q + 1];
             for (auto& kv : key) {
-                const int c = (int)(kv.first >> 40);
-                if (cls_start[q * STILE_NCLS1 + c] > r) cls_start[q * STILE_NCLS1 + c] = (int)r;
                 order[r] = kv.second;
                 perm[kv.second] = (int)r;
                 ++r;
             }
-            // empty classes start where the next non-empty one does
-            for (int c = STILE_NCLS1 - 2; c >= 0; --c)
-                cls_start[q * STILE_NCLS1 + c] =
-                    std::min(cls_start[q * STILE_NCLS1 + c], cls_start[q * STILE_NCLS1 + c + 1]);
         }
     }
     std::vector<int4> items;
@@ -539,7 +528,6 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
         SPTB_LAUNCHED();
     }
     SPTB_CUDA(cudaStreamSynchronize(p->stream));
-    if (sp.slot_mode && !cls_start.empty()) SPTB_TRY(build_stiles(p, cx, cy, rp, col, order, cnt, cls_start));
     return SPTB_OK;
 }
 
@@ -707,9 +695,12 @@ int build_matrices(sptb_plan* p, const sptb_geometry* g, const sptb_kernel* k) {
 
 // ---------------------------------------------------------------- filter fold
 
+// S diag(w) on S's pattern; with threshold > 0 the folded entries with
+// |w v| <= threshold are zeroed, as the reference prunes its weighted build
+// (gridding.py:146-163)
 template <typename C, typename R>
 __global__ void k_fold(const int* col, const C* v, C* out, const R* w, long long wlen,
-                       long long N, int P, long long nnz) {
+                       long long N, int P, long long nnz, double thr) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nnz;
          i += (long long)gridDim.x * blockDim.x) {
         const long long s = col[i];
@@ -717,6 +708,7 @@ __global__ void k_fold(const int* col, const C* v, C* out, const R* w, long long
         C c = v[i];
         c.x *= f;
         c.y *= f;
+        if (thr > 0 && !(hypot((double)c.x, (double)c.y) > thr)) c.x = c.y = 0;
         out[i] = c;
     }
 }
@@ -749,7 +741,6 @@ int fold_filter(sptb_plan* p) {
         p->SW_val = nullptr;
     }
     SPTB_TRY(upload_weights(p));
-    SPTB_TRY(fold_slot_filter(p));
     if (p->w_len == 0) return SPTB_OK;
     SPTB_CUDA(cudaMalloc(&p->SW_val, cs * (nnz > 0 ? nnz : 1)));
     if (nnz == 0) return SPTB_OK;
@@ -758,11 +749,11 @@ int fold_filter(sptb_plan* p) {
     if (p->prec == SPTB_PREC_F64)
         k_fold<double2, double><<<grid_of(nnz), 256, 0, p->stream>>>(
             p->S.col, (const double2*)p->S.val, (double2*)p->SW_val, (const double*)p->w_dev,
-            p->w_len, p->N, p->P, nnz);
+            p->w_len, p->N, p->P, nnz, p->threshold);
     else
         k_fold<float2, float><<<grid_of(nnz), 256, 0, p->stream>>>(
             p->S.col, (const float2*)p->S.val, (float2*)p->SW_val, (const float*)p->w_dev,
-            p->w_len, p->N, p->P, nnz);
+            p->w_len, p->N, p->P, nnz, p->threshold);
     SPTB_LAUNCHED();
     return SPTB_OK;
 }

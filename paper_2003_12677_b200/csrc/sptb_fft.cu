@@ -1278,7 +1278,7 @@ const float2* twiddles(sptb_plan* p, int logn) {
 }
 
 bool col_tma_ok(const void* g) {
-    return tmap_encoder() != nullptr && ((uintptr_t)g % 16) == 0 && !getenv("SPTB_NO_TMA");
+    return tmap_encoder() != nullptr && ((uintptr_t)g % 16) == 0 && !switches().no_tma;
 }
 
 // G [b][y][x] complex64 as a 3-D tensor of 8-byte elements; box CW2 x 256 x 1
@@ -1311,7 +1311,7 @@ int run_col(const CUtensorMap& tm, float2* g, int X, long long M, int strips, in
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int nstrip = nb * strips;
     const size_t buf = sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2);
-    if (COLP_BUFS * buf <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+    if (COLP_BUFS * buf <= 227 * 1024 && !switches().fft2_no_persist) {
         const int sm = (int)(COLP_BUFS * buf);
         SPTB_CUDA(set_smem_once((const void*)k_fft2_col_pers<LOGN, INV>, sm, SPTB_FFT_CARVEOUT));
         k_fft2_col_pers<LOGN, INV><<<(unsigned)std::min(nstrip, sm_count()), NT, sm, st>>>(tm, strips, nstrip, tw);
@@ -1364,7 +1364,7 @@ int col_launch_fwd(sptb_plan* p, float2* g, int nb, cudaStream_t st) {
 // the deapodization plane is applied from its separable factors (plan->deapo_xy)
 bool row_bulk_ok(const void* a, const void* g) {
     return ((uintptr_t)a % 16) == 0 && ((uintptr_t)g % 16) == 0 &&
-           !getenv("SPTB_FFT2_NO_BULK");
+           !switches().fft2_no_bulk;
 }
 
 template <int LOGN, bool INV>
@@ -1417,7 +1417,7 @@ int row_pack_launch(sptb_plan* p, const float* in, const float* plane, int64_t n
     constexpr int NT = RB2 * (1 << LOGN) / 16;
     if (row_bulk_ok(in, g)) {
         const int smp = (int)((COLP_BUFS * 8 * RB2 + 4) * (1 << LOGN));
-        if (smp <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+        if (smp <= 227 * 1024 && !switches().fft2_no_persist) {
             const int nstrip = (int)((long long)B * p->Y / RB2);
             SPTB_CUDA(set_smem_once((const void*)k_fft2_row_pack_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
             k_fft2_row_pack_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
@@ -1448,7 +1448,7 @@ int row_launch(sptb_plan* p, const float2* g, const float* plane, float scale, f
     constexpr int NT = RB2 * (1 << LOGN) / 16;
     if (row_bulk_ok(out, g)) {
         const int smp = (int)((COLP_BUFS * 8 * RB2 + 4) * (1 << LOGN));
-        if (smp <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+        if (smp <= 227 * 1024 && !switches().fft2_no_persist) {
             const int nstrip = (int)((long long)nb * p->Y / RB2);
             SPTB_CUDA(set_smem_once((const void*)k_fft2_row_unpack_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
             k_fft2_row_unpack_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
@@ -1498,7 +1498,7 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
                cudaStream_t st) {
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
     if constexpr (LOGN >= 9) {
-        if (!getenv("SPTB_FFT1_STOCKHAM")) {
+        if (!switches().fft1_stockham) {
 #ifndef SPTB_FFT1_BG
 #define SPTB_FFT1_BG 4
 #endif
@@ -1507,7 +1507,7 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
             if (B % BG == 0) {
                 constexpr int NT = BG * (1 << LOGN) / 16;
                 const size_t smb = sizeof(float2) * BG * (1 << LOGN);
-                if (!(fmt & SPTB_FMT_COMPLEX) && ((uintptr_t)in % 16) == 0 && !getenv("SPTB_FFT1_NO_BULK")) {
+                if (!(fmt & SPTB_FMT_COMPLEX) && ((uintptr_t)in % 16) == 0 && !switches().fft1_no_bulk) {
                     SPTB_CUDA(set_smem_once((const void*)k_fft1r_fwd<LOGN, BG, true>, (int)smb));
                     k_fft1r_fwd<LOGN, BG, true><<<dim3((unsigned)(B / BG), (unsigned)p->T), NT, smb, st>>>(
                         (const float*)in, 0, n, u0, nb, p->T, g_fwd_perm, (const float2*)p->tw1, (float2*)q, B);
@@ -1541,7 +1541,7 @@ int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n
                cudaStream_t st) {
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
     if constexpr (LOGN >= 9) {
-        if (getenv("SPTB_FFT1_R16_INV")) {  // measured: the Stockham inverse is faster (gathered input)
+        if (switches().fft1_r16_inv) {  // measured: the Stockham inverse is faster (gathered input)
             constexpr int NT = FBG * (1 << LOGN) / 16;
             SPTB_CUDA(set_smem_once((const void*)k_fft1r_inv<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
             k_fft1r_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), NT, sm, st>>>(
@@ -1564,7 +1564,7 @@ int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n
 // usable: complex64 plan, f32 caller data, n_p = 2^k in [128, 4096], B a multiple of FBG
 bool fft1_fused_ok(const sptb_plan* p, int fmt, int B) {
     return p->prec == SPTB_PREC_F32 && !(fmt & SPTB_FMT_F64) && fft1_log2(p) > 0 && B % FBG == 0 &&
-           !getenv("SPTB_NO_FUSED_FFT1");
+           !switches().no_fused_fft1;
 }
 
 int launch_fft1_fwd(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int nb, int B, void* q,
@@ -1600,7 +1600,7 @@ int launch_fft1_inv(sptb_plan* p, const void* q, int B, void* out, int fmt, int6
 // [512, 4096] (the row kernel owns whole rows: Y * nb a multiple of RB2)
 bool fft2_fused_ok(const sptb_plan* p, int fmt) {
     return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->X) > 0 &&
-           log2_fft(p->Y) > 0 && !getenv("SPTB_NO_FUSED_FFT2");
+           log2_fft(p->Y) > 0 && !switches().no_fused_fft2;
 }
 
 int launch_fft2_inv_unpack(sptb_plan* p, void* g, const void* plane, double scale, void* out, int64_t n,
@@ -1651,7 +1651,7 @@ int launch_fft2_pack_fwd(sptb_plan* p, const void* in, const void* plane, int64_
 // in-place unnormalised 2-D FFT of nb planes [b][y][x] (cuFFT's sign convention)
 bool fft2_inplace_ok(const sptb_plan* p, const void* g) {
     return p->prec == SPTB_PREC_F32 && log2_fft(p->X) > 0 && log2_fft(p->Y) > 0 && col_tma_ok(g) &&
-           !getenv("SPTB_NO_FUSED_FFT2");
+           !switches().no_fused_fft2;
 }
 
 int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_t st) {
@@ -1661,7 +1661,7 @@ int launch_fft2_inplace(sptb_plan* p, void* g, int nb, bool inverse, cudaStream_
 bool fft1_inv_tma_ok(const sptb_plan* p, const void* q, const void* out, int fmt, int B) {
     return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->P) > 0 &&
            B % CW2 == 0 && col_tma_ok(q) && ((uintptr_t)out % 16) == 0 &&
-           !getenv("SPTB_NO_FUSED_FFT1") && !getenv("SPTB_FFT1_INV_GATHER");
+           !switches().no_fused_fft1 && !switches().fft1_inv_gather;
 }
 
 // Q [s][b] complex64 (s in sample order) as a 2-D tensor of 8-byte elements;
@@ -1686,7 +1686,7 @@ int fwd_col_launch(sptb_plan* p, const void* in, int64_t n, int64_t u0, int nb, 
     SPTB_TRY(q_tmap(p, q, B, &tm));
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
-    if (COLP_BUFS * sm <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+    if (COLP_BUFS * sm <= 227 * 1024 && !switches().fft2_no_persist) {
         const int smp = COLP_BUFS * sm, nstrip = (B / CW2) * p->T;
         SPTB_CUDA(set_smem_once((const void*)k_fft1_fwd_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
         k_fft1_fwd_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(
@@ -1714,8 +1714,8 @@ int launch_fft1_fwd_tma(sptb_plan* p, const void* in, int64_t n, int64_t u0, int
 
 bool fft1_fwd_tma_ok(const sptb_plan* p, const void* in, const void* q, int fmt, int B) {
     return p->prec == SPTB_PREC_F32 && !(fmt & (SPTB_FMT_F64 | SPTB_FMT_COMPLEX)) && log2_fft(p->P) > 0 &&
-           B % CW2 == 0 && col_tma_ok(q) && ((uintptr_t)in % 16) == 0 && !getenv("SPTB_NO_FUSED_FFT1") &&
-           !getenv("SPTB_FFT1_FWD_ROWS");
+           B % CW2 == 0 && col_tma_ok(q) && ((uintptr_t)in % 16) == 0 && !switches().no_fused_fft1 &&
+           !switches().fft1_fwd_rows;
 }
 
 template <int LOGN>
@@ -1726,7 +1726,7 @@ int inv_col_launch(sptb_plan* p, const void* q, int B, void* out, int64_t n, int
     SPTB_TRY(q_tmap(p, q, B, &tm));
     constexpr int NT = CW2 * (1 << LOGN) / 16;
     const int sm = (int)(sizeof(float2) * CW2 * ((1 << LOGN) + 16 / CW2));
-    if (COLP_BUFS * sm <= 227 * 1024 && !getenv("SPTB_FFT2_NO_PERSIST")) {
+    if (COLP_BUFS * sm <= 227 * 1024 && !switches().fft2_no_persist) {
         const int smp = COLP_BUFS * sm, ngrp = (nb + CW2 - 1) / CW2, nstrip = ngrp * p->T;
         SPTB_CUDA(set_smem_once((const void*)k_fft1_inv_pers<LOGN>, smp, SPTB_FFT_CARVEOUT));
         k_fft1_inv_pers<LOGN><<<(unsigned)std::min(nstrip, sm_count()), NT, smp, st>>>(

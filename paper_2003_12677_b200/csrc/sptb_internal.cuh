@@ -111,19 +111,10 @@ struct PatchSH {
     int* s_colp = nullptr;    // S column indices renumbered to s'
 };
 
-// S (grid <- samples) by output tiles = the 8x8 cells of a sample patch.  A
-// tile needs the samples centred in its 10x10 centre box: its own patch and
-// an edge column/row or corner of each neighbour -- at most STILE_RUNS
-// contiguous s' runs thanks to the border-class order of build_patches.  The
-// staged runs are indexed by a centre table: for each box cell, the (begin,
-// count) of its samples in the staged list.  Tiles with more than STILE_CAP
-// samples (the dense centre) use a CSR gather; cells touched by irregular
-// samples get a deterministic fix-up pass.
-constexpr int STILE = 8;
-constexpr int STILE_RUNS = 10;
-constexpr int STILE_CAP = 192;
-constexpr int STILE_NCLS1 = 10;  // 9 border classes + end
-inline int stile_class(int lx, int ly) {  // TL T TR R BR B BL L interior
+// Sample border class inside its patch (TL T TR R BR B BL L interior): the
+// within-patch sample order of build_patches groups samples by it.
+constexpr int PATCH_NCLS = 9;
+inline int border_class(int lx, int ly) {
     const bool l = lx == 0, r = lx == PATCH_W - 1, t = ly == 0, b = ly == PATCH_W - 1;
     if (t) return l ? 0 : (r ? 2 : 1);
     if (b) return r ? 4 : (l ? 6 : 5);
@@ -131,23 +122,30 @@ inline int stile_class(int lx, int ly) {  // TL T TR R BR B BL L interior
     if (l) return 7;
     return 8;
 }
-struct alignas(16) STileMeta {
-    int2 run[STILE_RUNS];        // {s' begin, count}
-    unsigned table[100];         // centre box cell -> begin | count << 16 (staged list)
-    int ns, pad0, pad1, pad2;
+
+// Schedule of the row-segment S kernel (sptb_spmm_s.cu), built once per plan
+// from S's row pointers: tiles of short rows and the long rows.
+struct SSeg {
+    bool built = false;
+    int n_tiles = 0, n_long = 0;
+    int4* tiles = nullptr;  // {row begin, row end, first pair record, pair records}
+    int* longs = nullptr;   // long row ids, longest first
+    unsigned long long* pairs = nullptr;  // per tile, its rows by length in pairs (packed)
 };
 
-struct STiles {
-    int n_sparse = 0, n_dense = 0;
-    int* sparse = nullptr;       // tile (= patch) ids for the staged kernel
-    int* dense = nullptr;        // tile ids for the CSR-gather kernel
-    STileMeta* meta = nullptr;   // per patch
-    int n_fix = 0;               // cells touched by irregular samples (outside dense tiles)
-    int* fix_cell = nullptr;     // grid cell m
-    int* fix_ptr = nullptr;      // n_fix + 1
-    int2* fix_ent = nullptr;     // {s', slot}
-    void* swval = nullptr;       // slot rows with the filter folded (w[s] * sval)
+// Path-selection switches (tests and A/B measurements only): read from the
+// environment once, and again on sptb_reload_switches().
+struct Switches {
+    bool no_tma = false, no_fused_fft1 = false, no_fused_fft2 = false;
+    bool fft2_no_persist = false, fft2_no_bulk = false;
+    bool fft1_stockham = false, fft1_no_bulk = false, fft1_r16_inv = false;
+    bool fft1_inv_gather = false, fft1_fwd_rows = false, fft1_perm = false;
+    bool sirt_unfused = false, spmm_rows = false;
+    int sh_grid = 0;       // S^H launch grid override (0: default)
+    int pipe_chunks = 0;   // host pipeline chunks per call (0: default)
 };
+const Switches& switches();
+void reload_switches();
 
 struct FFTPlans {
     cufftHandle fft2 = 0;   // Y x X, batch B, [b][y][x]
@@ -169,12 +167,15 @@ struct sptb_plan {
 
     sptb::DevCSR S, SH;        // S: M x N rows=grid, SH: N x M rows=samples
     sptb::PatchSH shp;         // patch-grouped S^H (the production forward SpMM)
-    sptb::STiles stl;          // output-tiled S (the production adjoint SpMM)
+    sptb::SSeg sseg;           // row-segment S schedule (the production adjoint SpMM)
     void* SW_val = nullptr;    // S values with the filter folded (nullptr: none)
     std::vector<double> w_host;  // filter weights (n_p or N), empty = none
     void* w_dev = nullptr;       // real weights of plan precision (n_p or N)
     int64_t w_len = 0;
     double calib = 1.0;
+    void* wspec_dev = nullptr;          // sptb_spectral_apply weights (N entries, plan precision)
+    std::vector<double> wspec_host;     // what wspec_dev holds
+    std::vector<float> wspec_f32;       // complex64 plans: upload staging
 
     void* deapo = nullptr;     // M real (plan precision), row-major [y][x]
     float* deapo_xy = nullptr; // separable factors: (-1)^(x-X/2)/kx(x) [X], then (-1)^(y-Y/2)/ky(y) [Y]
@@ -253,16 +254,14 @@ int launch_transpose_permute(const void* in_bs, void* out_sb, const int* perm, i
 template <typename R>
 int launch_transpose_unpermute(const void* in_sb, void* out_bs, const int* order, int B, int64_t N,
                                cudaStream_t st);
-// Y[b][m] = S_(w) X, X [s'][b]: output-tiled kernel when the slot layout
-// exists (vals == S.val -> slot rows, vals == SW_val -> w-folded slot rows),
-// else the row-gather kernel over S with columns renumbered to s'
+// Y[b][m] = S_(w) X (vals = S.val or SW_val): the row-segment kernel for a
+// complex64 32-vector batch, else the row-gather kernel.  X [s'][b] (patch
+// order, columns renumbered) or, for _sample, X [s][b] (sample order).
 template <typename R>
-int launch_spmm_s(const sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B,
-                  cudaStream_t st);
-int build_stiles(sptb_plan* p, const std::vector<int>& cx, const std::vector<int>& cy,
-                 const std::vector<int>& rp, const std::vector<int>& col, const std::vector<int>& order,
-                 const std::vector<int64_t>& cnt, const std::vector<int>& cls_start);
-int fold_slot_filter(sptb_plan* p);
+int launch_spmm_s(sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B, cudaStream_t st);
+template <typename R>
+int launch_spmm_s_sample(sptb_plan* p, const void* vals, const void* x_sb, void* y_bm, int B,
+                         cudaStream_t st);
 // S with columns renumbered to the patch order s'
 inline DevCSR s_permuted(const sptb_plan* p) {
     DevCSR A = p->S;

@@ -572,7 +572,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {  // shared with sptb_fft.cu
 bool tma_ok(const sptb_plan* p, const void* x) {
     const size_t cs = p->csize;
     return p->shp.slot_mode && tmap_encoder() != nullptr && ((uintptr_t)x % 16) == 0 &&
-           ((size_t)p->X * cs) % 16 == 0 && ((size_t)p->M * cs) % 16 == 0 && !getenv("SPTB_NO_TMA");
+           ((size_t)p->X * cs) % 16 == 0 && ((size_t)p->M * cs) % 16 == 0 && !switches().no_tma;
 }
 
 template <typename R, int G, int CPL>
@@ -628,11 +628,8 @@ static int sh_slot_dispatch(const sptb_plan* p, const void* x, void* y, const vo
     constexpr int XS_BYTES = (BB * SLOT_PS * (int)sizeof(C) + 15) & ~15;
     const size_t sm = XS_BYTES + (size_t)PATCH_ITEM_ROWS * SLOT_STRIDE * sizeof(C);
     if (sp.n_items > 0) {
-        // persistent two-stage pipeline (default) or one item per CTA
-        static const bool one_per_cta = [] {
-            const char* e = getenv("SPTB_SH_GRID");
-            return !(e && e[0] == 'p');
-        }();
+        // one item per CTA (measured faster here than a persistent two-stage pipeline)
+        constexpr bool one_per_cta = true;
         const int stage = (int)((sm + 127) & ~(size_t)127);
         const size_t smt = one_per_cta ? sm : 2 * (size_t)stage;
         auto run = [&](auto kern) -> int {
@@ -672,11 +669,8 @@ static int sh_patch_dispatch(const sptb_plan* p, const void* x, void* y, const v
     if (sp.n_items == 0) return SPTB_OK;
     constexpr int BB = G * CPL;
     const PatchStage sg = patch_stage<R>(BB, sp.bw, sp.max_item_nnz);
-    // persistent two-stage pipeline (default) or one item per CTA (single stage)
-    static const bool one_per_cta = [] {
-        const char* e = getenv("SPTB_SH_GRID");
-        return e && e[0] == 'i';
-    }();
+    // persistent two-stage pipeline
+    constexpr bool one_per_cta = false;
     const size_t sm = (one_per_cta ? 1 : 2) * (size_t)sg.bytes;
     auto run = [&](auto kern) -> int {
         static int dev_cached = -1, per_sm = 0;

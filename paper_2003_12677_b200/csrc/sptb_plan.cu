@@ -12,6 +12,46 @@
 
 namespace sptb {
 
+// ---------------------------------------------------------------- switches
+namespace {
+Switches g_switches;
+bool g_switches_read = false;
+bool env_on(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] && e[0] != '0';
+}
+int env_int(const char* name) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : 0;
+}
+}  // namespace
+
+void reload_switches() {
+    Switches s;
+    s.no_tma = env_on("SPTB_NO_TMA");
+    s.no_fused_fft1 = env_on("SPTB_NO_FUSED_FFT1");
+    s.no_fused_fft2 = env_on("SPTB_NO_FUSED_FFT2");
+    s.fft2_no_persist = env_on("SPTB_FFT2_NO_PERSIST");
+    s.fft2_no_bulk = env_on("SPTB_FFT2_NO_BULK");
+    s.fft1_stockham = env_on("SPTB_FFT1_STOCKHAM");
+    s.fft1_no_bulk = env_on("SPTB_FFT1_NO_BULK");
+    s.fft1_r16_inv = env_on("SPTB_FFT1_R16_INV");
+    s.fft1_inv_gather = env_on("SPTB_FFT1_INV_GATHER");
+    s.fft1_fwd_rows = env_on("SPTB_FFT1_FWD_ROWS");
+    s.fft1_perm = env_on("SPTB_FFT1_PERM");
+    s.sirt_unfused = env_on("SPTB_SIRT_UNFUSED");
+    s.spmm_rows = env_on("SPTB_SPMM_ROWS");
+    s.pipe_chunks = std::max(0, env_int("SPTB_PIPE_CHUNKS"));
+    g_switches = s;
+    g_switches_read = true;
+}
+
+const Switches& switches() {
+    if (!g_switches_read) reload_switches();
+    return g_switches;
+}
+
+
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
 static std::atomic<long long> g_ffts{0};
@@ -176,12 +216,12 @@ static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void*
     int64_t chunk = p->max_batch;
     if (!din || !dout) {
         // host buffers: split into pipeline chunks so H2D, kernels and D2H overlap;
-        // the first chunk's H2D and the last one's D2H stay exposed
-        static const int64_t nchunks = [] {
-            const char* e = getenv("SPTB_PIPE_CHUNKS");
-            return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)32;  // measured e2e: 8 -> 2.76K, 16 -> 2.82K, 32 -> 2.85K slices/s
-        }();
-        chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, (units + nchunks - 1) / nchunks));
+        // the first chunk's H2D and the last one's D2H stay exposed.  Chunks
+        // are multiples of 4 units so the fused FFT passes run (B % 4 == 0).
+        const int64_t nchunks = switches().pipe_chunks > 0 ? switches().pipe_chunks : 8;
+        chunk = (units + nchunks - 1) / nchunks;
+        if (switches().pipe_chunks <= 0) chunk = (std::max<int64_t>(chunk, 4) + 3) / 4 * 4;
+        chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, chunk));
     }
     SPTB_TRY(ensure_work(p, pow2_at_least((int)std::min<int64_t>(chunk, units))));
     if (din && dout) {
@@ -271,14 +311,14 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
     SPTB_TRY(get_fft(p, B, &f));
     cudaStream_t st = p->stream;
     const void* vals = (filtered && p->SW_val) ? p->SW_val : p->S.val;
-    if (fft1_fused_ok(p, in_fmt, B) && !getenv("SPTB_FFT1_PERM")) {
+    if (fft1_fused_ok(p, in_fmt, B) && !switches().fft1_perm) {
         // pack + FFT1 in one pass, rows left in sample order: the row gather
         // of S reads them through its original column indices (no permutation)
         if (fft1_fwd_tma_ok(p, in, p->S1, in_fmt, B))
             SPTB_TRY(launch_fft1_fwd_tma(p, in, n, u0, nb, B, p->S1, st));
         else
             SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st, false));
-        SPTB_TRY(launch_spmm<R>(p->S, vals, p->S1, p->G0, B, true, nullptr, st));
+        SPTB_TRY(launch_spmm_s_sample<R>(p, vals, p->S1, p->G0, B, st));
     } else {
         if (fft1_fused_ok(p, in_fmt, B)) {  // pack + FFT1 + permute in one pass
             SPTB_TRY(launch_fft1_fwd(p, in, in_fmt, n, u0, nb, B, p->S1, st));
@@ -296,14 +336,14 @@ int iradon_batch(sptb_plan* p, bool filtered, double scale, const void* in, int 
 }
 
 template <typename R>
-int weights_batch(sptb_plan* p, const void* in, int in_fmt, int64_t n, int64_t u0, int nb, int B,
-                  void* out, int out_fmt, int64_t on, int64_t ou0) {
+int weights_batch(sptb_plan* p, const void* w, int64_t wlen, const void* in, int in_fmt, int64_t n,
+                  int64_t u0, int nb, int B, void* out, int out_fmt, int64_t on, int64_t ou0) {
     FFTPlans* f;
     SPTB_TRY(get_fft(p, B, &f));
     cudaStream_t st = p->stream;
     SPTB_TRY(launch_pack<R>(in, in_fmt, n, u0, nb, B, p->N, nullptr, p->S0, st));
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_FORWARD));
-    if (p->w_len) SPTB_TRY(launch_weight_sino<R>(p->S0, p->w_dev, p->w_len, p->P, p->N, B, st));
+    if (wlen) SPTB_TRY(launch_weight_sino<R>(p->S0, w, wlen, p->P, p->N, B, st));
     SPTB_TRY(exec_fft(p, f->fft1, p->S0, CUFFT_INVERSE));
     return launch_unpack<R>(p->S0, p->N, nullptr, 1.0 / p->P, out, out_fmt, on, ou0, nb, st);
 }
@@ -381,6 +421,11 @@ int sptb_plan_create(sptb_plan** out, const sptb_geometry* g, const sptb_kernel*
     return SPTB_OK;
 }
 
+int sptb_reload_switches(void) {
+    sptb::reload_switches();
+    return SPTB_OK;
+}
+
 int sptb_plan_destroy(sptb_plan* p) {
     if (!p) return SPTB_OK;
     cudaSetDevice(p->device);
@@ -392,9 +437,8 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->SW_val, p->w_dev, p->deapo, p->deapo_xy, p->G0, p->G1, p->G2, p->S0, p->S1,
                     p->stage_in, p->stage_out, p->red, p->fft_work,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
-                    p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->stl.sparse,
-                    p->stl.dense, p->stl.meta, p->stl.fix_cell, p->stl.fix_ptr, p->stl.fix_ent,
-                    p->stl.swval, p->tw1};
+                    p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->sseg.tiles,
+                    p->sseg.longs, p->sseg.pairs, p->wspec_dev, p->tw1};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->twn)
@@ -558,23 +602,28 @@ int sptb_spectral_apply(sptb_plan* p, const double* w, int64_t nw, const void* i
     if (nw != p->P && nw != p->N)
         return fail(SPTB_ERR_SHAPE, "weights fit neither (n_p,) nor (N,)");
     cudaSetDevice(p->device);
-    // temporarily swap in the caller's weights
-    std::vector<double> keep_w = p->w_host;
-    void* keep_dev = p->w_dev;
-    void* keep_sw = p->SW_val;
-    const int64_t keep_len = p->w_len;
-    p->w_dev = nullptr;
-    p->SW_val = nullptr;
-    p->w_host.assign(w, w + nw);
-    int rc = upload_weights(p);
-    if (rc == SPTB_OK) rc = sptb_apply_weights(p, in, in_fmt, out, out_fmt, n);
-    SPTB_CUDA(cudaStreamSynchronize(p->stream));
-    if (p->w_dev) cudaFree(p->w_dev);
-    p->w_host = keep_w;
-    p->w_dev = keep_dev;
-    p->SW_val = keep_sw;
-    p->w_len = keep_len;
-    return rc;
+    // the caller's weights go to a plan-owned buffer (sized once for N
+    // entries, re-uploaded only when they change): no allocation per call
+    const size_t rs = p->prec == SPTB_PREC_F64 ? 8 : 4;
+    if (!p->wspec_dev) SPTB_CUDA(cudaMalloc(&p->wspec_dev, rs * (size_t)p->N));
+    if (p->wspec_host.size() != (size_t)nw || !std::equal(w, w + nw, p->wspec_host.begin())) {
+        p->wspec_host.assign(w, w + nw);
+        if (rs == 8) {
+            SPTB_CUDA(cudaMemcpyAsync(p->wspec_dev, p->wspec_host.data(), 8 * nw, cudaMemcpyHostToDevice,
+                                      p->stream));
+        } else {
+            p->wspec_f32.resize(nw);
+            for (int64_t i = 0; i < nw; ++i) p->wspec_f32[i] = (float)w[i];
+            SPTB_CUDA(cudaMemcpyAsync(p->wspec_dev, p->wspec_f32.data(), 4 * nw, cudaMemcpyHostToDevice,
+                                      p->stream));
+        }
+    }
+    return drive(p, in, in_fmt, p->N, out, out_fmt, p->N, n,
+                 [&](const void* s, int64_t nl, int64_t ul, void* d, int64_t onl, int64_t oul,
+                     int nb, int B) {
+                     return DISPATCH(p, weights_batch, p, p->wspec_dev, nw, s, in_fmt, nl, ul, nb, B, d,
+                                     out_fmt, onl, oul);
+                 });
 }
 
 int sptb_apply_weights(sptb_plan* p, const void* in, int32_t in_fmt, void* out, int32_t out_fmt,
@@ -584,8 +633,8 @@ int sptb_apply_weights(sptb_plan* p, const void* in, int32_t in_fmt, void* out, 
     return drive(p, in, in_fmt, p->N, out, out_fmt, p->N, n,
                  [&](const void* s, int64_t nl, int64_t ul, void* d, int64_t onl, int64_t oul,
                      int nb, int B) {
-                     return DISPATCH(p, weights_batch, p, s, in_fmt, nl, ul, nb, B, d, out_fmt,
-                                     onl, oul);
+                     return DISPATCH(p, weights_batch, p, p->w_dev, p->w_len, s, in_fmt, nl, ul, nb, B,
+                                     d, out_fmt, onl, oul);
                  });
 }
 

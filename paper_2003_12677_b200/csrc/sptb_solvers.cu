@@ -1363,7 +1363,7 @@ struct Solver {
 
     // fused SIRT update + x pass (complex64, fused FFT2 usable, S^H via TMA)
     bool sirt_fused_ok() const {
-        return sizeof(R) == 4 && fft2_inplace_ok(p, W) && tma_ok(p, W) && !getenv("SPTB_SIRT_UNFUSED");
+        return sizeof(R) == 4 && fft2_inplace_ok(p, W) && tma_ok(p, W) && !switches().sirt_unfused;
     }
     int sirt_update_forward(int nonneg) {
         if constexpr (sizeof(R) == 4) {

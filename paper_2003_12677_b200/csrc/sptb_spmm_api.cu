@@ -165,8 +165,10 @@ __global__ void k_fill_pattern(C* x, long long n) {
     }
 }
 
-// the launches the operators issue: S^H = patch kernel over [b][m] -> [s'][b];
-// S / S diag(w) = gather kernel over [s'][b] -> [b][m] (TRANS epilogue)
+// exactly the launches gridrec / radon issue: S^H = patch kernel over [b][m]
+// with rows written in sample order (radon's TMA inverse FFT1 reads them);
+// S / S diag(w) = the S kernel over [s][b] (sample order, after the fused
+// FFT1) -> [b][m]
 template <typename R>
 int time_spmm(sptb_plan* p, int which, int B, int reps, double* ms) {
     using C = typename CplxT<R>::T;
@@ -183,8 +185,8 @@ int time_spmm(sptb_plan* p, int which, int B, int reps, double* ms) {
     k_fill_pattern<C><<<gridn(nx), 256, 0, p->stream>>>(x, nx);
     SPTB_LAUNCHED();
     auto launch = [&]() -> int {
-        if (adjoint) return launch_spmm_sh_patch<R>(p, x, y, B, nullptr, p->stream);
-        return launch_spmm_s<R>(p, vals, x, y, B, p->stream);
+        if (adjoint) return launch_spmm_sh_patch<R>(p, x, y, B, nullptr, p->stream, tma_ok(p, x));
+        return launch_spmm_s_sample<R>(p, vals, x, y, B, p->stream);
     };
     for (int w = 0; w < 2; ++w) SPTB_TRY(launch());
     cudaEvent_t e0, e1;

@@ -236,6 +236,11 @@ class DeviceGridCSR:
 
     @property
     def nnz(self) -> int:
+        # the filtered matrix shares S's pattern on the device; its reference
+        # counterpart drops the entries the folded weights zero (or push to
+        # <= threshold), so its nnz comes from the pruned host view
+        if self.filtered:
+            return int(self.matrix.nnz)
         return self._nnz
 
     def _fetch(self):
@@ -260,6 +265,11 @@ class DeviceGridCSR:
         coo_r = np.repeat(mf, lens)
         S = sp.csr_matrix((vals, (coo_r, ci[: self._nnz])), shape=self.shape)
         S.sum_duplicates()
+        if self.filtered:  # the reference's folded build prunes |w v| <= threshold (gridding.py:159-163)
+            thr = self._plan.threshold
+            if thr > 0:
+                S.data[np.abs(S.data) <= thr] = 0.0
+            S.eliminate_zeros()
         S.sort_indices()
         SH = S.conj().T.tocsr()
         SH.sort_indices()
@@ -399,21 +409,55 @@ class TomoOperators:
         return w.reshape(self.geom.sino_shape)
 
     def precondition(self, sino):
-        return _spectral(self._plan, sino, np.sqrt(self.spectral_weights))
+        return precondition_apply(Preconditioner(weights=self.spectral_weights), sino, self)
 
     def apply_weights(self, sino):
         return _spectral(self._plan, sino, self.spectral_weights)
 
 
+_SPECTRAL_PLANS: dict = {}
+
+
+def _spectral_plan(n_theta: int, n_p: int, like) -> _Plan:
+    """A device plan for detector-axis spectral passes over (n_theta, n_p)
+    sinograms, cached per (shape, precision, device): precondition_apply has
+    no operator bundle in the reference's signature."""
+    prec = _lib.PREC_F64
+    if _is_cuda_tensor(like) and like.dtype in (torch.float32, torch.complex64):
+        prec = _lib.PREC_F32
+    dev = like.device.index if _is_cuda_tensor(like) else _default_device()
+    key = (int(n_theta), int(n_p), prec, dev)
+    plan = _SPECTRAL_PLANS.get(key)
+    if plan is None:
+        plan = _Plan(ScanGeometry(n_p=int(n_p), n_theta=int(n_theta)), KernelSpec(), prec, 8, dev, 0.0)
+        _SPECTRAL_PLANS[key] = plan
+    return plan
+
+
 def precondition_apply(pre: Preconditioner, sino, ops: TomoOperators | None = None):
-    """Spectrum times sqrt(weights) (operators.py:108-121).  Needs a plan of
-    matching geometry: pass ``ops`` (the reference's signature has none)."""
-    sh = np.shape(sino)
-    if sh[-1] != pre.weights.shape[-1]:
-        raise ShapeMismatchError(f"sinogram last axis {sh[-1]} != weights {pre.weights.shape[-1]}")
-    if ops is None:
-        raise ValueError("precondition_apply needs ops= (a plan for the sinogram geometry)")
-    return _spectral(ops._plan, sino, np.sqrt(pre.weights))
+    """Half-power preconditioner: detector-axis spectrum times sqrt(weights)
+    (operators.py:108-121).  Same signature as the reference; the FFT pair
+    runs on the device through ``ops``' plan when given (and of matching
+    shape), else through a cached plan for the sinogram's shape.  Weights
+    may be radial (n_p,) or per sample, shaped like the sinogram."""
+    sh = tuple(np.shape(sino))
+    if len(sh) == 0 or sh[-1] != pre.weights.shape[-1]:
+        raise ShapeMismatchError(f"sinogram last axis {sh[-1] if sh else None} != weights "
+                                 f"{pre.weights.shape[-1]}")
+    w = np.sqrt(pre.weights)
+    x = sino
+    if len(sh) == 1:  # one detector row
+        x = sino[None]
+    shape2 = tuple(np.shape(x))[-2:]
+    if w.ndim > 1 and tuple(w.shape) != shape2:
+        raise ShapeMismatchError(f"weights shape {w.shape} != sinogram {shape2}")
+    plan = ops._plan if ops is not None and tuple(ops.geom.sino_shape) == shape2 else None
+    if plan is None:
+        plan = _spectral_plan(shape2[0], shape2[1], x)
+    wc = np.ascontiguousarray(w, dtype=np.float64).ravel()
+    out = _apply(plan, lib.sptb_spectral_apply, x, shape2, shape2, "sinogram",
+                 extra=(wc.ctypes.data_as(C.POINTER(C.c_double)), int(wc.size)))
+    return out[0] if len(sh) == 1 else out
 
 
 def _default_device():

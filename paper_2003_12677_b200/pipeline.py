@@ -33,7 +33,12 @@ class SinogramStack:
     geometry: ScanGeometry
 
     def __post_init__(self):
-        d = np.asarray(self.data, dtype=np.float64)
+        # float32 / float64 arrays (and memory maps of volume files) are kept
+        # as they are -- a 512-slice 2048 x 1536 stack is 6.4 GB in float32;
+        # anything else becomes float64 like the reference's
+        d = self.data
+        if not (isinstance(d, np.ndarray) and d.dtype in (np.float32, np.float64)):
+            d = np.asarray(d, dtype=np.float64)
         if d.ndim != 3:
             raise ShapeMismatchError(f"sinogram stack must be 3D, got {d.shape}")
         want = (self.geometry.n_z,) + tuple(self.geometry.sino_shape)
@@ -156,8 +161,8 @@ def _device_solver(ops, cfg):
     """(slices tensor/array (k, T, P)) -> (rec, final residual, iters, conv, status) per unit."""
     from .solvers import solve_batch
 
-    def run(data):
-        rec, reps, stat = solve_batch(data, ops, cfg, raise_on_failure=False)
+    def run(data, out=None):
+        rec, reps, stat = solve_batch(data, ops, cfg, raise_on_failure=False, out=out)
         final = [r.residual_history[-1] if r.residual_history else 0.0 for r in reps]
         iters = [r.iterations_run for r in reps]
         conv = [r.converged for r in reps]
@@ -166,40 +171,81 @@ def _device_solver(ops, cfg):
 
 
 def run_pipeline(stack: SinogramStack, cfg, workers: int = 1, ops=None, max_per_pass: int = 8,
-                 *, group=None, solver=None):
+                 *, group=None, solver=None, out=None):
     """Reconstruct every slice (pipeline.py:179-235).
 
     Single process: all pair units go through the device solver in batches
     (``workers`` / ``max_per_pass`` only define the task ranges reported by
     WorkerFailureError, exactly as in the reference).  Under an initialised
     torch.distributed group of size G > 1, rank r solves its contiguous unit
-    range on its own GPU; rank 0 returns the assembled stack, other ranks
-    return ``(None, report)``.  ``solver`` overrides the per-rank solve
-    (used by the CPU multi-process tests).
+    range on its own GPU:
+
+    * input: when every rank passes the stack (e.g. a memory map of the same
+      SPTOMO01 file), each rank copies only its own slices host -> device over
+      its own PCIe link; otherwise rank 0's stack is scattered with NCCL
+      point-to-point sends (other ranks may pass ``stack=None``);
+    * output: when every rank passes ``out`` (a host (n_z, n_y, n_x) array all
+      ranks can write, e.g. a memory-mapped output volume), each rank writes
+      its own slices device -> host; otherwise the slices are gathered to
+      rank 0 over NCCL.
+
+    Rank 0 returns the assembled stack (``out`` when given); other ranks
+    return ``(None, report)``.  ``solver`` overrides the per-rank solve (used
+    by the CPU multi-process tests).
     """
     t0 = time.perf_counter()
-    geom = stack.geometry
-    if ops is None and solver is None:
-        from .operators import build_operators
-        ops = build_operators(geom, filter_kind=cfg.filter_kind())
-    solve_fn = solver or _device_solver(ops, cfg)
-    n_z = stack.n_z
-    n_units = (n_z + 1) // 2
-
     dist = _dist_group(group)
     if dist is None:
-        rec, final, iters, conv, stat = solve_fn(stack.data)
+        if stack is None:
+            raise ValueError("run_pipeline needs a stack outside a process group")
+        geom = stack.geometry
+        if ops is None and solver is None:
+            from .operators import build_operators
+            ops = build_operators(geom, filter_kind=cfg.filter_kind())
+        solve_fn = solver or _device_solver(ops, cfg)
+        n_z = stack.n_z
+        n_units = (n_z + 1) // 2
+        direct = out is not None and solver is None and isinstance(stack.data, np.ndarray)
+        if direct:  # results straight into the caller's (e.g. memory-mapped) volume
+            rec, final, iters, conv, stat = solve_fn(stack.data, out=out)
+        else:
+            rec, final, iters, conv, stat = solve_fn(stack.data)
+        bad = [u for u in range(n_units) if stat[u] != 0]
+        if bad and workers == 1:
+            # one worker: the reference solves in-process, so the solver's own
+            # exception reaches the caller (pipeline.py:201-204)
+            from .solvers import _EXC
+            u = bad[0]
+            lo, hi = unit_slices(u, 1, n_z)
+            raise _EXC.get(stat[u], RuntimeError)(
+                f"{cfg.algorithm} failed on slices [{lo}, {hi}) (device status {stat[u]})")
         err = _failure(stat, n_units, n_z, workers, max_per_pass,
                        {u: _cause(stat[u], cfg.algorithm) for u in range(n_units)})
         if err is not None:
             raise err
-        out = np.asarray(rec, dtype=np.float64)
+        if out is not None:
+            if not direct:
+                out[...] = np.asarray(rec.cpu().numpy() if hasattr(rec, "cpu") else rec)
+            vol = out
+        else:
+            vol = np.asarray(rec.cpu().numpy() if hasattr(rec, "cpu") else rec, dtype=np.float64)
         from .solvers import SolverReport
         rep = SolverReport(residual_history=[float(f) for f in final],
                            iterations_run=int(max(iters)) if iters else 0,
                            converged=all(conv), wall_time=time.perf_counter() - t0)
-        return TomogramStack(data=out), rep
-    return _run_distributed(stack, cfg, solve_fn, dist, t0, workers, max_per_pass)
+        return TomogramStack(data=vol), rep
+    if ops is None and solver is None:
+        from .operators import build_operators
+        ops = build_operators(stack.geometry if stack is not None else _bcast_geometry(None, dist),
+                              filter_kind=cfg.filter_kind())
+    solve_fn = solver or _device_solver(ops, cfg)
+    f64 = ops is not None and ops.plan.precision == _f64_precision()
+    return _run_distributed(stack, cfg, solve_fn, dist, t0, workers, max_per_pass, f64, out)
+
+
+def _f64_precision():
+    from . import _lib
+    return _lib.PREC_F64
 
 
 def _dist_group(group):
@@ -214,71 +260,132 @@ def _dist_group(group):
     return group if group is not None else tdist.group.WORLD
 
 
-def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass):
+def _bcast_geometry(stack, group):
+    """Rank 0's (n_z, n_theta, n_p, n_y, n_x, center) and angles to every rank."""
+    import torch
+    import torch.distributed as tdist
+    dev = _dist_device(group)
+    hdr = torch.zeros(6, dtype=torch.float64, device=dev)
+    if tdist.get_rank(group) == 0:
+        g = stack.geometry
+        hdr[:] = torch.tensor([stack.n_z, g.n_theta, g.n_p, g.n_y, g.n_x, g.center], dtype=torch.float64)
+    tdist.broadcast(hdr, _root(group), group)
+    n_z, T, P, Y, X, c = hdr.tolist()
+    ang = torch.empty(int(T), dtype=torch.float64, device=dev)
+    if tdist.get_rank(group) == 0:
+        ang.copy_(torch.as_tensor(np.asarray(stack.geometry.angles, dtype=np.float64)))
+    tdist.broadcast(ang, _root(group), group)
+    return ScanGeometry(n_p=int(P), n_theta=int(T), angles=ang.cpu().numpy(), n_z=int(n_z), n_x=int(X),
+                        n_y=int(Y), center=float(c))
+
+
+def _root(group):
+    import torch.distributed as tdist
+    return tdist.get_global_rank(group, 0) if group is not None and group != tdist.group.WORLD else 0
+
+
+def _dist_device(group):
+    import torch
+    import torch.distributed as tdist
+    if tdist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _h2d(host, lo, hi, dtype, dev):
+    """Slices [lo, hi) of a host stack -> device tensor (pinned staging)."""
+    import torch
+    part = np.ascontiguousarray(host[lo:hi], dtype=np.float64 if dtype == torch.float64 else np.float32)
+    t = torch.from_numpy(part)
+    if dev.type == "cuda":
+        return t.pin_memory().to(dev, non_blocking=True)
+    return t.clone()
+
+
+def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64=False, out=None):
     import torch
     import torch.distributed as tdist
 
     from .solvers import SolverReport
 
     rank, world = tdist.get_rank(group), tdist.get_world_size(group)
-    backend = tdist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    geom = stack.geometry
-    n_z = stack.n_z
+    root = _root(group)
+    dev = _dist_device(group)
+    dt = torch.float64 if f64 else torch.float32
+    # every rank learns the geometry and which side holds the data
+    flags = torch.tensor([1.0 if stack is not None else 0.0, 1.0 if out is not None else 0.0],
+                         dtype=torch.float64, device=dev)
+    tdist.all_reduce(flags, op=tdist.ReduceOp.MIN, group=group)
+    local_in, local_out = flags[0].item() > 0, flags[1].item() > 0
+    geom = stack.geometry if local_in else _bcast_geometry(stack, group)
+    n_z = stack.n_z if local_in else geom.n_z
     n_units = (n_z + 1) // 2
     T, P = geom.sino_shape
     Y, X = geom.grid_shape
     ranges = rank_ranges(n_units, world)
     spans = [unit_slices(u0, ul, n_z) if ul > 0 else (0, 0) for u0, ul in ranges]
-
-    # ---- scatter: rank 0 -> ranks (NCCL P2P over NVLink; no native scatter)
     lo, hi = spans[rank]
-    mine = torch.empty((hi - lo, T, P), dtype=torch.float32, device=dev)
-    ops_ = []
-    if rank == 0:
-        full = torch.from_numpy(np.ascontiguousarray(stack.data, dtype=np.float32)).to(dev)
-        for r in range(1, world):
-            a, b = spans[r]
-            if b > a:
-                ops_.append(tdist.P2POp(tdist.isend, full[a:b].contiguous(), r, group))
-        mine.copy_(full[lo:hi])
-    elif hi > lo:
-        ops_.append(tdist.P2POp(tdist.irecv, mine, 0, group))
-    if ops_:
-        for w in tdist.batch_isend_irecv(ops_):
-            w.wait()
+
+    # ---- input: own range over this rank's PCIe link, or rank 0 -> ranks over NCCL
+    if local_in:
+        mine = _h2d(stack.data, lo, hi, dt, dev)
+    else:
+        mine = torch.empty((hi - lo, T, P), dtype=dt, device=dev)
+        ops_ = []
+        if rank == 0:
+            for r in range(1, world):
+                a, b = spans[r]
+                if b > a:
+                    ops_.append(tdist.P2POp(tdist.isend, _h2d(stack.data, a, b, dt, dev),
+                                            tdist.get_global_rank(group, r) if group is not tdist.group.WORLD else r,
+                                            group))
+            mine.copy_(_h2d(stack.data, lo, hi, dt, dev))
+        elif hi > lo:
+            ops_.append(tdist.P2POp(tdist.irecv, mine, root, group))
+        if ops_:
+            for w in tdist.batch_isend_irecv(ops_):
+                w.wait()
 
     # ---- solve (no collective inside)
     ul = ranges[rank][1]
     if ul > 0:
         rec, final, iters, conv, stat = solve_fn(mine)
-        rec = torch.as_tensor(rec, device=dev).to(torch.float32)
+        rec = torch.as_tensor(rec, device=dev).to(dt)
     else:
-        rec = torch.empty((0, Y, X), dtype=torch.float32, device=dev)
+        rec = torch.empty((0, Y, X), dtype=dt, device=dev)
         final, iters, conv, stat = [], [], [], []
     meta = torch.tensor([[f, i, float(c), float(s)] for f, i, c, s in zip(final, iters, conv, stat)],
                         dtype=torch.float64, device=dev).reshape(-1, 4)
 
-    # ---- gather: ranks -> rank 0
+    # ---- output: own range device -> host, or ranks -> rank 0 over NCCL
+    vol = None
+    if local_out:
+        if hi > lo:
+            out[lo:hi] = rec.cpu().numpy()
     ops_ = []
+    metas = [None] * world
     if rank == 0:
-        vol = torch.empty((n_z, Y, X), dtype=torch.float32, device=dev)
-        metas = [None] * world
-        vol[lo:hi].copy_(rec)
+        if not local_out:
+            vol = torch.empty((n_z, Y, X), dtype=dt, device=dev)
+            vol[lo:hi].copy_(rec)
         metas[0] = meta
         for r in range(1, world):
             a, b = spans[r]
             if b > a:
-                buf = vol[a:b]
-                ops_.append(tdist.P2POp(tdist.irecv, buf, r, group))
+                src = tdist.get_global_rank(group, r) if group is not tdist.group.WORLD else r
+                if not local_out:
+                    ops_.append(tdist.P2POp(tdist.irecv, vol[a:b], src, group))
                 metas[r] = torch.empty((ranges[r][1], 4), dtype=torch.float64, device=dev)
-                ops_.append(tdist.P2POp(tdist.irecv, metas[r], r, group))
+                ops_.append(tdist.P2POp(tdist.irecv, metas[r], src, group))
     elif hi > lo:
-        ops_.append(tdist.P2POp(tdist.isend, rec.contiguous(), 0, group))
-        ops_.append(tdist.P2POp(tdist.isend, meta, 0, group))
+        if not local_out:
+            ops_.append(tdist.P2POp(tdist.isend, rec.contiguous(), root, group))
+        ops_.append(tdist.P2POp(tdist.isend, meta, root, group))
     if ops_:
         for w in tdist.batch_isend_irecv(ops_):
             w.wait()
+    if local_out:
+        tdist.barrier(group)  # every rank's slices are in ``out``
 
     # ---- failure decision is shared so every rank raises the same error
     flag = torch.zeros(3, dtype=torch.float64, device=dev)
@@ -290,7 +397,7 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass):
             u = int(bad[0])
             r = next(i for i, (u0, ln) in enumerate(ranges) if u0 <= u < u0 + ln)
             flag[0], flag[1], flag[2] = 1.0, float(r), float(stat_all[u])
-    tdist.broadcast(flag, 0, group)
+    tdist.broadcast(flag, root, group)
     if flag[0].item() > 0:
         r = int(flag[1].item())
         raise WorkerFailureError(spans[r], _cause(int(flag[2].item()), cfg.algorithm))
@@ -300,4 +407,5 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass):
                        iterations_run=int(allm[:, 1].max()) if len(allm) else 0,
                        converged=bool(np.all(allm[:, 2] > 0)),
                        wall_time=time.perf_counter() - t0)
-    return TomogramStack(data=vol.cpu().numpy().astype(np.float64)), rep
+    data = out if local_out else vol.cpu().numpy().astype(np.float64)
+    return TomogramStack(data=data), rep

@@ -68,13 +68,17 @@ class SolverReport:
 _EXC = {_lib.ERR_DIVERGENCE: DivergenceError, _lib.ERR_NONFINITE: NonFiniteError}
 
 
-def solve_batch(sino, ops: TomoOperators, cfg: SolverConfig, raise_on_failure: bool = True):
+def solve_batch(sino, ops: TomoOperators, cfg: SolverConfig, raise_on_failure: bool = True,
+                out=None):
     """Solve every unit of ``sino`` ((..., n_theta, n_p), real slices paired
     (2k, 2k+1) or complex pairs) in device batches.
 
     Returns ``(rec, reports, status)``: one SolverReport and one status code
     per unit (0 ok, or the DivergenceError / NonFiniteError code).  With
     ``raise_on_failure`` the first failing unit raises its exception type.
+    ``out``: for host input, a float32 / float64 array of the result's shape
+    to write into (e.g. a memory-mapped output volume) instead of a new
+    float64 array.
     """
     t0 = time.perf_counter()
     g = ops.geom
@@ -101,13 +105,29 @@ def solve_batch(sino, ops: TomoOperators, cfg: SolverConfig, raise_on_failure: b
         if a.ndim < 2 or a.shape[-2:] != g.sino_shape:
             raise ShapeMismatchError(f"sinogram shape {a.shape} != {g.sino_shape}")
         cplx = np.iscomplexobj(a)
-        a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
-        fmt = _lib.FMT_F64 | (_lib.FMT_COMPLEX if cplx else _lib.FMT_REAL)
+        # float32 host stacks go in as they are (no float64 copy); results
+        # are float64 / complex128 like the reference's
+        if a.dtype == (np.complex64 if cplx else np.float32):
+            a = np.ascontiguousarray(a)
+            fmt_in = _lib.FMT_F32
+        else:
+            a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+            fmt_in = _lib.FMT_F64
+        kind = _lib.FMT_COMPLEX if cplx else _lib.FMT_REAL
         lead = a.shape[:-2]
-        out = np.empty(lead + g.grid_shape, dtype=a.dtype)
+        fmt_o = _lib.FMT_F64
+        if out is None:
+            out = np.empty(lead + g.grid_shape, dtype=np.complex128 if cplx else np.float64)
+        else:
+            want = (np.complex64, np.complex128) if cplx else (np.float32, np.float64)
+            if out.shape != lead + g.grid_shape or out.dtype not in want or not out.flags.c_contiguous:
+                raise ShapeMismatchError(f"out must be a C-contiguous {lead + g.grid_shape} array of "
+                                         f"{'/'.join(str(np.dtype(d)) for d in want)}")
+            fmt_o = _lib.FMT_F32 if out.dtype in (np.float32, np.complex64) else _lib.FMT_F64
         plan.bind_stream(0)
         src, dst = a.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)
         t = a
+        fmt = None
     n = int(np.prod(lead)) if lead else 1
     units = n if cplx else (n + 1) // 2
     iters_cap = 1 if cfg.algorithm == "fbp" else int(cfg.max_iter)
@@ -115,7 +135,9 @@ def solve_batch(sino, ops: TomoOperators, cfg: SolverConfig, raise_on_failure: b
     its = np.zeros(max(units, 1), dtype=np.int32)
     conv = np.zeros(max(units, 1), dtype=np.int32)
     stat = np.zeros(max(units, 1), dtype=np.int32)
-    rc = lib.sptb_solve(plan.h, C.byref(cfg_c), src, fmt, dst, fmt, n,
+    fmt_out = fmt if fmt is not None else fmt_o | kind
+    fmt_src = fmt if fmt is not None else fmt_in | kind
+    rc = lib.sptb_solve(plan.h, C.byref(cfg_c), src, fmt_src, dst, fmt_out, n,
                         hist.ctypes.data_as(C.c_void_p), its.ctypes.data_as(C.c_void_p),
                         conv.ctypes.data_as(C.c_void_p), stat.ctypes.data_as(C.c_void_p))
     if rc not in (_lib.OK, _lib.ERR_DIVERGENCE, _lib.ERR_NONFINITE):

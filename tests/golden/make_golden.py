@@ -165,6 +165,52 @@ def cgs_case(sp):
     return out
 
 
+def precondition_case(sp):
+    """precondition_apply / TomoOperators.precondition / preconditioner
+    (operators.py:85-121,262-290): radial and per-sample weights, real and
+    complex sinograms, a sinogram of another angle count, one detector row."""
+    geom = sp.ScanGeometry(n_p=32, n_theta=20)
+    rng = np.random.default_rng(9)
+    s = rng.standard_normal(geom.sino_shape)
+    sc = s + 1j * rng.standard_normal(geom.sino_shape)
+    out = dict(s=s, sc=sc)
+    for kind in ("hamming", "ramlak", "none"):
+        ops = sp.build_operators(geom, filter_kind="ramlak")
+        pre = ops.preconditioner(kind)
+        out[f"pre_{kind}_w"] = pre.weights
+        out[f"pre_{kind}_s"] = sp.precondition_apply(pre, s)
+        out[f"pre_{kind}_sc"] = sp.precondition_apply(pre, sc)
+    ops_h = sp.build_operators(geom, filter_kind="hamming")
+    out["ops_hamming_precondition_s"] = ops_h.precondition(s)
+    wfull = rng.uniform(0.0, 2.0, geom.sino_shape)
+    pre = sp.Preconditioner(weights=wfull)
+    out["wfull"] = wfull
+    out["pre_full_sc"] = sp.precondition_apply(pre, sc)
+    s7 = rng.standard_normal((7, 32))
+    out["s7"] = s7
+    out["pre_hamming_s7"] = sp.precondition_apply(ops.preconditioner("hamming"), s7)
+    out["pre_hamming_row"] = sp.precondition_apply(ops.preconditioner("hamming"), s7[3])
+    return out
+
+
+def threshold_case(sp):
+    """build_operators(..., threshold=0.05) (operators.py:317-371,
+    gridding.py:159-195): both matrices pruned, the filtered one on its
+    weighted values; operators and calibration on the pruned matrices."""
+    geom = sp.ScanGeometry(n_p=32, n_theta=20)
+    ops = sp.build_operators(geom, filter_kind="ramlak", threshold=0.05)
+    rng = np.random.default_rng(11)
+    u = rng.standard_normal(geom.grid_shape)
+    s = rng.standard_normal(geom.sino_shape)
+    out = dict(u=u, s=s, calib=ops.calib_scale, radon_u=ops.radon(u), iradon_s=ops.iradon(s),
+               adj_s=ops.radon_adjoint(s))
+    for tag, m in (("S", ops.csr), ("SF", ops.csr_filtered)):
+        out[f"{tag}_row_ptr"] = m.row_ptr
+        out[f"{tag}_col"] = m.col_idx
+        out[f"{tag}_vals"] = m.vals
+    return out
+
+
 def pipeline_case(sp):
     """run_pipeline on an odd 5-slice stack (test_pipeline.py:131-136)."""
     geom = sp.ScanGeometry(n_p=32, n_theta=12, n_z=5)
@@ -218,6 +264,14 @@ def main():
     np.savez_compressed(os.path.join(OUT, "solvers_cgs_g32.npz"), **cgs_case(sp))
     print("wrote cgs")
     if "--cgs-only" in sys.argv:
+        return
+    np.savez_compressed(os.path.join(OUT, "precond_g32.npz"), **precondition_case(sp))
+    print("wrote precond")
+    if "--precond-only" in sys.argv:
+        return
+    np.savez_compressed(os.path.join(OUT, "threshold_g32.npz"), **threshold_case(sp))
+    print("wrote threshold")
+    if "--threshold-only" in sys.argv:
         return
     for name, gkw, kkw in GEOMS:
         d = operators_case(sp, name, gkw, kkw)

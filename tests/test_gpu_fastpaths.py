@@ -33,16 +33,22 @@ def sb():
 
 
 def _env(name, value):
+    """Set an SPTB_* path switch for the block (the library reads the switches
+    once; sptb_reload_switches re-reads them)."""
+    from paper_2003_12677_b200 import _lib
+
     class _E:
         def __enter__(self):
             self.old = os.environ.get(name)
             os.environ[name] = value
+            _lib.lib.sptb_reload_switches()
 
         def __exit__(self, *a):
             if self.old is None:
                 os.environ.pop(name, None)
             else:
                 os.environ[name] = self.old
+            _lib.lib.sptb_reload_switches()
     return _E()
 
 

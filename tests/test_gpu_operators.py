@@ -185,3 +185,55 @@ def test_near_zero_deapodization_raises(sb):
     with pytest.raises(sb.NearZeroDenominatorError):
         sb.build_operators(sb.ScanGeometry(n_p=16, n_theta=4),
                            kernel=sb.KernelSpec(width=5, beta=0.75 * math.pi))
+
+
+def test_precondition_matches_reference(sb):
+    """precondition_apply(pre, sino) with the reference's signature (no ops:
+    a cached device plan for the sinogram's shape), TomoOperators.precondition
+    and preconditioner(kind) against the unmodified reference
+    (operators.py:85-121,262-290); complex128 plans for NumPy input, a
+    complex64 plan for float32 device tensors."""
+    import torch
+    d = load_golden("precond_g32.npz")
+    geom = sb.ScanGeometry(n_p=32, n_theta=20)
+    ops = sb.build_operators(geom, filter_kind="ramlak")
+    for kind in ("hamming", "ramlak", "none"):
+        pre = ops.preconditioner(kind)
+        np.testing.assert_array_equal(pre.weights, d[f"pre_{kind}_w"])
+        assert rel(sb.precondition_apply(pre, d["s"]), d[f"pre_{kind}_s"]) <= 1e-12
+        out = sb.precondition_apply(pre, d["sc"])
+        assert np.iscomplexobj(out) and rel(out, d[f"pre_{kind}_sc"]) <= 1e-12
+        assert rel(sb.precondition_apply(pre, d["s"], ops), d[f"pre_{kind}_s"]) <= 1e-12
+    ops_h = sb.build_operators(geom, filter_kind="hamming")
+    assert rel(ops_h.precondition(d["s"]), d["ops_hamming_precondition_s"]) <= 1e-12
+    pre = sb.Preconditioner(weights=d["wfull"])
+    assert rel(sb.precondition_apply(pre, d["sc"]), d["pre_full_sc"]) <= 1e-12
+    hpre = ops.preconditioner("hamming")
+    assert rel(sb.precondition_apply(hpre, d["s7"]), d["pre_hamming_s7"]) <= 1e-12
+    row = sb.precondition_apply(hpre, d["s7"][3])
+    assert row.shape == (32,) and rel(row, d["pre_hamming_row"]) <= 1e-12
+    t = torch.tensor(d["s"], dtype=torch.float32, device="cuda")
+    out = sb.precondition_apply(hpre, t)
+    assert out.is_cuda and out.dtype == torch.float32
+    assert rel(out.cpu().numpy(), d["pre_hamming_s"]) <= 1e-5
+    with pytest.raises(sb.ShapeMismatchError):
+        sb.precondition_apply(hpre, np.zeros((20, 31)))
+
+
+@pytest.mark.parametrize("prec,tol", [("complex128", 1e-10), ("complex64", 1e-4)])
+def test_threshold_build_matches_reference(sb, prec, tol):
+    """threshold > 0 (gridding.py:159-163): S pruned on |v|, the filtered
+    matrix on its weighted values |w v| -- structure identical to the
+    reference's, and the operators and calibration built on them."""
+    d = load_golden("threshold_g32.npz")
+    ops = sb.build_operators(sb.ScanGeometry(n_p=32, n_theta=20), filter_kind="ramlak",
+                             threshold=0.05, precision=prec)
+    for tag, m in (("S", ops.csr), ("SF", ops.csr_filtered)):
+        np.testing.assert_array_equal(m.row_ptr, d[f"{tag}_row_ptr"])
+        np.testing.assert_array_equal(m.col_idx, d[f"{tag}_col"])
+        assert rel(m.vals, d[f"{tag}_vals"]) <= min(tol, 1e-6)
+        assert m.nnz == len(d[f"{tag}_vals"])
+    assert abs(ops.calib_scale - float(d["calib"])) <= tol * abs(float(d["calib"]))
+    assert rel(ops.radon(d["u"]), d["radon_u"]) <= tol
+    assert rel(ops.radon_adjoint(d["s"]), d["adj_s"]) <= tol
+    assert rel(ops.iradon(d["s"]), d["iradon_s"]) <= tol

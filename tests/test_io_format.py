@@ -1,5 +1,6 @@
-"""SPTOMO01 volume files and the io helpers against fixtures written by the
-unmodified reference (io.py:35-193)."""
+"""SPTOMO01 volume files against fixtures written by the unmodified
+reference (io.py:35-89): byte-identical writes, validated (memory-mapped)
+reads, the streamed writer and the corruption checks."""
 
 import os
 
@@ -14,8 +15,11 @@ def test_read_reference_volumes():
     v = io.read_volume(os.path.join(GOLDEN, "vol_sino.sptomo"))
     assert v.kind == io.KIND_SINOGRAM and v.data.shape == (3, 5, 8) and v.center == 3.5
     np.testing.assert_allclose(v.angles, np.linspace(0, np.pi, 5, endpoint=False), rtol=0, atol=0)
-    g = io.sinogram_geometry(v)
-    assert (g.n_z, g.n_theta, g.n_p, g.center) == (3, 5, 8, 3.5)
+    assert isinstance(v.data, np.memmap) and v.data.dtype == np.float32
+    h = io.read_header(os.path.join(GOLDEN, "vol_sino.sptomo"))
+    assert h.shape == (3, 5, 8) and h.payload_offset == 8 + 45 + 8 * 5
+    w = io.read_volume(os.path.join(GOLDEN, "vol_sino.sptomo"), mmap=False)
+    np.testing.assert_array_equal(w.data, v.data)
     t = io.read_volume(os.path.join(GOLDEN, "vol_tomo.sptomo"))
     assert t.kind == io.KIND_TOMOGRAM and t.angles is None and t.data.shape == (2, 8, 8)
 
@@ -40,14 +44,31 @@ def test_corrupt_volumes(tmp_path):
             io.read_volume(p)
 
 
-def test_helpers_match_reference():
+def test_streamed_writer_matches_whole_write(tmp_path):
+    """Slices written out of order (as ranks / chunks finish) give the same
+    bytes as one write_volume; a second process-style attach writes into the
+    same in-progress file; an exception leaves no file behind."""
     from paper_2003_12677_b200 import io
-    d = load_golden("io_misc.npz")
-    np.testing.assert_array_equal(io.phantom_shepp_logan(16, 3), d["phantom"])
-    sino = io.read_volume(os.path.join(GOLDEN, "vol_sino.sptomo")).data
-    np.testing.assert_allclose(io.normalize(np.abs(sino) + 0.1, 2.0), d["norm"], rtol=1e-15)
-    with pytest.raises(Exception):
-        io.normalize(sino, 0.0)
+    v = io.read_volume(os.path.join(GOLDEN, "vol_sino.sptomo"))
+    out = str(tmp_path / "s.sptomo")
+    with io.VolumeWriter(out, v.kind, v.data.shape, center=v.center, angles=v.angles) as w:
+        w.write(2, v.data[2])
+        other = io.VolumeWriter.attach(w.tmp)
+        other[1] = v.data[1]
+        other.flush()
+        w.write(0, v.data[0:1])
+        assert not os.path.exists(out)
+    assert open(out, "rb").read() == open(os.path.join(GOLDEN, "vol_sino.sptomo"), "rb").read()
+    bad = str(tmp_path / "bad.sptomo")
+    with pytest.raises(RuntimeError):
+        with io.VolumeWriter(bad, io.KIND_TOMOGRAM, (2, 4, 4)) as w:
+            raise RuntimeError("boom")
+    assert not os.path.exists(bad) and not os.listdir(tmp_path) == []
+    assert all(not f.startswith("bad.sptomo") for f in os.listdir(tmp_path))
+    with pytest.raises(ValueError):
+        io.write_volume(str(tmp_path / "x"), io.KIND_SINOGRAM, np.zeros((2, 3, 4)))
+    with pytest.raises(ValueError):
+        io.write_volume(str(tmp_path / "x"), 7, np.zeros((2, 3, 4)))
 
 
 def test_geometry_helpers_against_oracle():

@@ -106,6 +106,19 @@ def test_solver_variants(sol):
     assert rel(r, sol["tv_mu_rec"]) <= 1e-10
 
 
+def test_precondition_matches_reference():
+    """precondition_apply (operators.py:108-121) for radial / per-sample
+    weights, real / complex input, other angle counts and one detector row."""
+    from oracle.tomo import op_precondition
+    d = load_golden("precond_g32.npz")
+    for kind in ("hamming", "ramlak", "none"):
+        w = d[f"pre_{kind}_w"]
+        assert rel(op_precondition(d["s"], w), d[f"pre_{kind}_s"]) <= 1e-13
+        assert rel(op_precondition(d["sc"], w), d[f"pre_{kind}_sc"]) <= 1e-13
+    assert rel(op_precondition(d["sc"], d["wfull"]), d["pre_full_sc"]) <= 1e-13
+    assert rel(op_precondition(d["s7"], d["pre_hamming_w"]), d["pre_hamming_s7"]) <= 1e-13
+
+
 CGS_TAGS = [("", dict(max_iter=8)), ("_nonneg", dict(max_iter=6, nonneg=True)),
             ("_tol", dict(max_iter=40, tol=0.02))]
 

@@ -51,12 +51,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n_z, bad_global_unit, out_q):
+def _worker(rank, world, port, n_z, bad_global_unit, out_q, mode="local", out_path=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        stack = _stack(n_z)
+        stack = _stack(n_z) if (mode != "scatter" or rank == 0) else None
+        out = None
+        if mode == "out":
+            out = np.memmap(out_path, dtype=np.float32, mode="r+", shape=(n_z, Y, X))
         n_units = (n_z + 1) // 2
         u0 = rank_ranges(n_units, world)[rank][0]
 
@@ -67,8 +70,9 @@ def _worker(rank, world, port, n_z, bad_global_unit, out_q):
             return rec, final, iters, conv, stat
 
         try:
-            vol, rep = run_pipeline(stack, SolverConfig(algorithm="sirt", max_iter=3), solver=solver)
-            out_q.put((rank, "ok", None if vol is None else vol.data, rep.residual_history,
+            vol, rep = run_pipeline(stack, SolverConfig(algorithm="sirt", max_iter=3), solver=solver,
+                                    out=out)
+            out_q.put((rank, "ok", None if vol is None else np.array(vol.data), rep.residual_history,
                        rep.iterations_run, rep.converged))
         except WorkerFailureError as e:
             out_q.put((rank, "fail", e.slice_range, str(e.cause), 0, False))
@@ -76,11 +80,12 @@ def _worker(rank, world, port, n_z, bad_global_unit, out_q):
         dist.destroy_process_group()
 
 
-def _run(world, n_z, bad=None):
+def _run(world, n_z, bad=None, mode="local", out_path=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n_z, bad, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_z, bad, q, mode, out_path))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
@@ -105,14 +110,22 @@ def test_rank_ranges_partition_units():
     assert unit_slices(2, 3, 9) == (4, 9)
 
 
+@pytest.mark.parametrize("mode", ["local", "scatter", "out"])
 @pytest.mark.parametrize("world,n_z", [(2, 7), (2, 8), (3, 11)])
-def test_distributed_matches_single_process(world, n_z):
-    """Scatter -> per-rank solve -> gather reproduces the single-process result
-    bit for bit, and the report aggregates units in slice order
-    (pipeline.py:223-234)."""
+def test_distributed_matches_single_process(world, n_z, mode, tmp_path):
+    """Per-rank solve of contiguous pair-unit ranges reproduces the
+    single-process result bit for bit, and the report aggregates units in
+    slice order (pipeline.py:223-234), for every data path: each rank loads
+    its own slices ("local"), rank 0 scatters over the process group
+    ("scatter", other ranks pass no stack), each rank writes its own slices
+    into a shared memory-mapped volume ("out")."""
     single_vol, single_rep = run_pipeline(_stack(n_z), SolverConfig(algorithm="sirt", max_iter=3),
                                           solver=_fake_solver())
-    res = _run(world, n_z)
+    out_path = None
+    if mode == "out":
+        out_path = str(tmp_path / "vol.f32")
+        np.memmap(out_path, dtype=np.float32, mode="w+", shape=(n_z, Y, X)).flush()
+    res = _run(world, n_z, mode=mode, out_path=out_path)
     rank0 = res[0]
     assert rank0[1] == "ok"
     # the fake solver runs per rank on float32-transported data: compare to the
