@@ -41,6 +41,7 @@ void reload_switches() {
     s.fft1_perm = env_on("SPTB_FFT1_PERM");
     s.sirt_unfused = env_on("SPTB_SIRT_UNFUSED");
     s.spmm_rows = env_on("SPTB_SPMM_ROWS");
+    s.spmm_tile_out = env_on("SPTB_SPMM_TILE_OUT");
     s.pipe_chunks = std::max(0, env_int("SPTB_PIPE_CHUNKS"));
     g_switches = s;
     g_switches_read = true;
@@ -214,14 +215,26 @@ static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void*
     is_device_ptr(out, &dout);
     const int64_t units = n_units(in_fmt, n);
     int64_t chunk = p->max_batch;
+    std::vector<int64_t> sizes;  // host buffers: pipeline chunk sizes in units
     if (!din || !dout) {
-        // host buffers: split into pipeline chunks so H2D, kernels and D2H overlap;
-        // the first chunk's H2D and the last one's D2H stay exposed.  Chunks
-        // are multiples of 4 units so the fused FFT passes run (B % 4 == 0).
-        const int64_t nchunks = switches().pipe_chunks > 0 ? switches().pipe_chunks : 8;
-        chunk = (units + nchunks - 1) / nchunks;
-        if (switches().pipe_chunks <= 0) chunk = (std::max<int64_t>(chunk, 4) + 3) / 4 * 4;
-        chunk = std::max<int64_t>(1, std::min<int64_t>(p->max_batch, chunk));
+        // split into pipeline chunks so H2D, kernels and D2H overlap.  The
+        // first chunk's H2D and the last one's D2H stay exposed, so those two
+        // are single units; the rest go in chunks of 4 units, the smallest
+        // batch the fused FFT passes take (B % 4 == 0).  SPTB_PIPE_CHUNKS=k
+        // overrides with k equal chunks.
+        if (switches().pipe_chunks > 0) {
+            const int64_t c = std::max<int64_t>(1, std::min<int64_t>(
+                p->max_batch, (units + switches().pipe_chunks - 1) / switches().pipe_chunks));
+            for (int64_t u = 0; u < units; u += c) sizes.push_back(std::min(c, units - u));
+        } else if (units >= 6) {
+            const int64_t c = std::min<int64_t>(4, p->max_batch);
+            sizes.push_back(1);
+            for (int64_t u = 1; u < units - 1; u += c) sizes.push_back(std::min(c, units - 1 - u));
+            sizes.push_back(1);
+        } else {
+            for (int64_t u = 0; u < units; ++u) sizes.push_back(1);
+        }
+        chunk = *std::max_element(sizes.begin(), sizes.end());
     }
     SPTB_TRY(ensure_work(p, pow2_at_least((int)std::min<int64_t>(chunk, units))));
     if (din && dout) {
@@ -235,10 +248,10 @@ static int drive(sptb_plan* p, const void* in, int in_fmt, int64_t in_len, void*
     const size_t sbi = slice_bytes(in_fmt, in_len), sbo = slice_bytes(out_fmt, out_len);
     SPTB_CUDA(cudaEventRecord(p->ev_start, p->stream));  // after earlier work on the plan stream
     SPTB_CUDA(cudaStreamWaitEvent(p->io_in, p->ev_start, 0));
-    int64_t i = 0;
-    for (int64_t u0 = 0; u0 < units; u0 += chunk, ++i) {
+    int64_t u0 = 0;
+    for (size_t i = 0; i < sizes.size(); u0 += sizes[i], ++i) {
         const int k = (int)(i % sptb_plan::NPIPE);
-        const int nb = (int)std::min<int64_t>(chunk, units - u0);
+        const int nb = (int)sizes[i];
         int64_t first, cnt;
         slice_range(in_fmt, n, u0, nb, &first, &cnt);
         const void* src = in;

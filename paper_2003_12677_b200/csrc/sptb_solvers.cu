@@ -173,28 +173,39 @@ __device__ __forceinline__ typename CT<R>::T rc(double x, double y) {
     return c;
 }
 
-// forward differences (solvers.py:308-314): last column / row zero
-__device__ __forceinline__ D2 grad_x(const D2* v, size_t i, long long m, int X) {
+// forward differences (solvers.py:308-314): last column / row zero.  V is
+// the storage type of the TV state (the plan's complex type); arithmetic is
+// fp64
+template <typename V>
+__device__ __forceinline__ D2 grad_x(const V* v, size_t i, long long m, int X) {
     if ((int)(m % X) == X - 1) return make_double2(0, 0);
-    const D2 a = v[i], b = v[i + 1];
+    const D2 a = d2(v[i]), b = d2(v[i + 1]);
     return make_double2(b.x - a.x, b.y - a.y);
 }
-__device__ __forceinline__ D2 grad_y(const D2* v, size_t i, long long m, int X, int Y) {
+template <typename V>
+__device__ __forceinline__ D2 grad_y(const V* v, size_t i, long long m, int X, int Y) {
     if ((int)(m / X) == Y - 1) return make_double2(0, 0);
-    const D2 a = v[i], b = v[i + X];
+    const D2 a = d2(v[i]), b = d2(v[i + X]);
     return make_double2(b.x - a.x, b.y - a.y);
 }
 // -div2d(vx, vy) (solvers.py:317-327), i.e. grad^T
-__device__ __forceinline__ D2 grad_t(const D2* vx, const D2* vy, size_t i, long long m, int X,
-                                     int Y) {
+template <typename V>
+__device__ __forceinline__ D2 grad_t(const V* vx, const V* vy, size_t i, long long m, int X, int Y) {
     // div2d(vx,vy)[y][x] = vx[x] (x<X-1) - vx[x-1] (x>0) + same along y; return its negative
     const int x = (int)(m % X), y = (int)(m / X);
     double re = 0, im = 0;
-    if (x < X - 1) { re += vx[i].x; im += vx[i].y; }
-    if (x > 0) { re -= vx[i - 1].x; im -= vx[i - 1].y; }
-    if (y < Y - 1) { re += vy[i].x; im += vy[i].y; }
-    if (y > 0) { re -= vy[i - X].x; im -= vy[i - X].y; }
+    if (x < X - 1) { re += (double)vx[i].x; im += (double)vx[i].y; }
+    if (x > 0) { re -= (double)vx[i - 1].x; im -= (double)vx[i - 1].y; }
+    if (y < Y - 1) { re += (double)vy[i].x; im += (double)vy[i].y; }
+    if (y > 0) { re -= (double)vy[i - X].x; im -= (double)vy[i - X].y; }
     return make_double2(-re, -im);
+}
+template <typename V>
+__device__ __forceinline__ V tv_store(double x, double y) {
+    V v;
+    v.x = x;
+    v.y = y;
+    return v;
 }
 
 // ------------------------------------------------------------------ grid ops
@@ -657,32 +668,15 @@ struct OpCgsDir {  // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
 
 // ------------------------------------------------------------------ grid ops (TV)
 
-// rho = (d - b) - grad u  (the stacked target minus fwd(u), unscaled; solvers.py:410-411,438)
-struct OpTvRho {
-    static constexpr int kUnroll = TV_UNROLL;
-    const D2 *u, *dx, *dy, *bx, *by;
-    D2 *rx, *ry;
-    int X, Y;
-    struct In { D2 gx, gy, dx, dy, bx, by; };
-    __device__ bool enabled(int) const { return true; }
-    __device__ In load(int, size_t i, long long m) const {
-        return In{grad_x(u, i, m, X), grad_y(u, i, m, X, Y), dx[i], dy[i], bx[i], by[i]};
-    }
-    __device__ void apply(int, size_t i, long long, const In& v, double (&)[1]) const {
-        rx[i] = make_double2(v.dx.x - v.bx.x - v.gx.x, v.dx.y - v.bx.y - v.gx.y);
-        ry[i] = make_double2(v.dy.x - v.by.x - v.gy.x, v.dy.y - v.by.y - v.gy.y);
-    }
-};
-
 // s = mu (deapo y scale) + lam grad^T(rho)   (adj(), solvers.py:397-399)
 // MODE 0: p = s, W = deapo p, acc <s,s>;  1: acc <s,s>;  2: p = s + beta p, W = deapo p
-template <typename R, int MODE>
+template <typename R, int MODE, typename V>
 struct OpTvS {
     static constexpr int kUnroll = TV_UNROLL;
     using C = typename CT<R>::T;
     C* w;
-    D2* p;
-    const D2 *rx, *ry;
+    V* p;
+    const V *rx, *ry;
     const R* deapo;
     double scale;
     const Unit* us;
@@ -693,7 +687,7 @@ struct OpTvS {
         In v;
         v.y = w[i];
         v.gt = grad_t(rx, ry, i, m, X, Y);
-        v.pp = MODE == 2 ? p[i] : D2{};
+        v.pp = MODE == 2 ? d2(p[i]) : D2{};
         v.d = deapo[m];
         return v;
     }
@@ -707,7 +701,7 @@ struct OpTvS {
             acc[1] += s.y * s.y;
         }
         if (MODE == 0) {
-            p[i] = s;
+            p[i] = tv_store<V>(s.x, s.y);
             w[i] = rc<R>(s.x * d, s.y * d);
         }
         if (MODE == 2) {
@@ -715,15 +709,16 @@ struct OpTvS {
             if (!un.inner_stop) {
                 pp.x = s.x + un.beta[0] * pp.x;
                 pp.y = s.y + un.beta[1] * pp.y;
-                p[i] = pp;
+                p[i] = tv_store<V>(pp.x, pp.y);
             }
             w[i] = rc<R>(pp.x * d, pp.y * d);
         }
     }
 };
 
+template <typename V>
 struct OpTvGradNorm {  // ||grad p||^2 per channel
-    const D2* p;
+    const V* p;
     const Unit* us;
     int X, Y;
     struct In { D2 gx, gy; };
@@ -737,16 +732,17 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     }
 };
 
+template <typename V>
 struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
     static constexpr int kUnroll = TV_UNROLL;
-    D2 *u, *rx, *ry;
-    const D2* p;
+    V *u, *rx, *ry;
+    const V* p;
     const Unit* us;
     int X, Y;
     struct In { D2 pp, gx, gy, x, a, c; };
     __device__ bool enabled(int b) const { return us[b].stepped; }
     __device__ In load(int, size_t i, long long m) const {
-        return In{p[i], grad_x(p, i, m, X), grad_y(p, i, m, X, Y), u[i], rx[i], ry[i]};
+        return In{d2(p[i]), grad_x(p, i, m, X), grad_y(p, i, m, X, Y), d2(u[i]), d2(rx[i]), d2(ry[i])};
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
         const Unit& un = us[b];
@@ -757,19 +753,22 @@ struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
         a.y -= un.alpha[1] * v.gx.y;
         c.x -= un.alpha[0] * v.gy.x;
         c.y -= un.alpha[1] * v.gy.y;
-        u[i] = x;
-        rx[i] = a;
-        ry[i] = c;
+        u[i] = tv_store<V>(x.x, x.y);
+        rx[i] = tv_store<V>(a.x, a.y);
+        ry[i] = tv_store<V>(c.x, c.y);
     }
 };
 
-// isotropic shrink + Bregman update (solvers.py:418-421, 330-341); W = deapo u
-template <typename R>
+// isotropic shrink + Bregman update (solvers.py:418-421, 330-341); W = deapo u.
+// Fused with the next outer iteration's stacked target (solvers.py:410-411):
+// d is used only there, so the pass writes rho = (d - b) - grad u (u is the
+// same) instead of d -- one fp64 grid pass less per outer iteration, and no d.
+template <typename R, typename V>
 struct OpTvShrink {
     static constexpr int kUnroll = TV_UNROLL;
     using C = typename CT<R>::T;
-    const D2* u;
-    D2 *dx, *dy, *bx, *by;
+    const V* u;
+    V *rx, *ry, *bx, *by;
     C* w;
     const R* deapo;
     const Unit* us;
@@ -777,7 +776,7 @@ struct OpTvShrink {
     struct In { D2 x, gx, gy, bx, by; R d; };
     __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const {
-        return In{u[i], grad_x(u, i, m, X), grad_y(u, i, m, X, Y), bx[i], by[i], deapo[m]};
+        return In{d2(u[i]), grad_x(u, i, m, X), grad_y(u, i, m, X, Y), d2(bx[i]), d2(by[i]), deapo[m]};
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
         const Unit& un = us[b];
@@ -795,10 +794,12 @@ struct OpTvShrink {
             ox[c] = vx[c] * f;
             oy[c] = vy[c] * f;
         }
-        dx[i] = make_double2(ox[0], ox[1]);
-        dy[i] = make_double2(oy[0], oy[1]);
-        bx[i] = make_double2(v.bx.x + v.gx.x - ox[0], v.bx.y + v.gx.y - ox[1]);
-        by[i] = make_double2(v.by.x + v.gy.x - oy[0], v.by.y + v.gy.y - oy[1]);
+        const D2 nbx = make_double2(v.bx.x + v.gx.x - ox[0], v.bx.y + v.gx.y - ox[1]);
+        const D2 nby = make_double2(v.by.x + v.gy.x - oy[0], v.by.y + v.gy.y - oy[1]);
+        bx[i] = tv_store<V>(nbx.x, nbx.y);
+        by[i] = tv_store<V>(nby.x, nby.y);
+        rx[i] = tv_store<V>(ox[0] - nbx.x - v.gx.x, ox[1] - nbx.y - v.gx.y);
+        ry[i] = tv_store<V>(oy[0] - nby.x - v.gy.x, oy[1] - nby.y - v.gy.y);
     }
 };
 
@@ -1234,7 +1235,7 @@ struct Solver {
     C *U = nullptr, *G = nullptr, *W = nullptr, *BH = nullptr, *RH = nullptr, *QH = nullptr;
     // float64 Krylov state (CGLS / TV)
     D2 *Ud = nullptr, *Pd = nullptr, *RHd = nullptr;
-    D2 *dx = nullptr, *dy = nullptr, *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;
+    C *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;  // TV: Bregman b, stacked target rho
     D2 *Rg = nullptr, *SHg = nullptr, *Qg = nullptr, *Hg = nullptr, *Vg = nullptr;  // CGS
     double *part = nullptr, *sums = nullptr, *sums2 = nullptr, *sums3 = nullptr, *hist = nullptr;
     Unit* us = nullptr;
@@ -1284,16 +1285,16 @@ struct Solver {
         SPTB_TRY(alloc((void**)&BH, sb));
         SPTB_TRY(alloc((void**)&RH, sb));
         SPTB_TRY(alloc((void**)&QH, sb));
-        if (algo == SPTB_ALGO_FBP || algo == SPTB_ALGO_SIRT) {
-            SPTB_TRY(alloc((void**)&U, gb));
-            SPTB_TRY(alloc((void**)&G, gb));
-        } else {
+        if (algo == SPTB_ALGO_CGLS) {
             SPTB_TRY(alloc((void**)&Ud, gd));
             SPTB_TRY(alloc((void**)&Pd, gd));
             SPTB_TRY(alloc((void**)&RHd, sd));
+        } else {  // FBP / SIRT / TV: iterate (and TV's p) in the plan's type
+            SPTB_TRY(alloc((void**)&U, gb));
+            SPTB_TRY(alloc((void**)&G, gb));
         }
         if (algo == SPTB_ALGO_TV) {
-            for (D2** q : {&dx, &dy, &bx, &by, &rx, &ry}) SPTB_TRY(alloc((void**)q, gd));
+            for (C** q : {&bx, &by, &rx, &ry}) SPTB_TRY(alloc((void**)q, gb));
         }
         if (algo == SPTB_ALGO_CGLS && cgs) {
             for (D2** q : {&Rg, &SHg, &Qg, &Hg, &Vg}) SPTB_TRY(alloc((void**)q, gd));
@@ -1323,7 +1324,7 @@ struct Solver {
         if (U) SPTB_CUDA(cudaMemsetAsync(U, 0, gb, st));
         if (Ud) SPTB_CUDA(cudaMemsetAsync(Ud, 0, gd, st));
         if (algo == SPTB_ALGO_TV)
-            for (D2* q : {dx, dy, bx, by}) SPTB_CUDA(cudaMemsetAsync(q, 0, gd, st));
+            for (C* q : {bx, by, rx, ry}) SPTB_CUDA(cudaMemsetAsync(q, 0, gb, st));  // u = d = b = 0: rho = 0
         return SPTB_OK;
     }
 
@@ -1627,44 +1628,43 @@ struct Solver {
             k_tv_mu<<<1, 64, 0, st>>>(us, sums3, 0.0, B);
         }
         SPTB_TRY(unit_kernel_done());
-        // u0 = 0 -> rho_a = b
-        SPTB_TRY(copy_bh_to_rhd());
+        // u0 = 0 -> rho_a = b.  The TV state (u = U, p = G, rho, b and the
+        // spectral residual RH) is stored in the plan's complex type with fp64
+        // arithmetic in every pass: the element passes are HBM-bound, and the
+        // stacked CGLS restarts every outer iteration after 2 steps
         SPTB_CUDA(cudaMemcpyAsync(RH, BH, sizeof(C) * (size_t)B * p->N, cudaMemcpyDeviceToDevice, st));
         const int inner = std::max(1, cfg.tv_inner_iter);
         for (int it = 0; it < cfg.max_iter; ++it) {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
-            // stacked CGLS on (sqrt(mu) A; sqrt(lam) grad) u = (sqrt(mu) b; sqrt(lam)(d - b))
-            SPTB_TRY(grid<0>(OpTvRho{Ud, dx, dy, bx, by, rx, ry, X, Y}, nullptr));
+            // stacked CGLS on (sqrt(mu) A; sqrt(lam) grad) u = (sqrt(mu) b; sqrt(lam)(d - b));
+            // rho = (d - b) - grad u comes from the previous shrink pass (0 at u = 0)
             SPTB_TRY(adjoint_grid(RH, true));
-            SPTB_TRY(grid<2>(OpTvS<R, 0>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, sums2));
+            SPTB_TRY(grid<2>(OpTvS<R, 0, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, sums2));
             k_tv_inner_begin<<<1, 64, 0, st>>>(us, sums2, B);
             SPTB_TRY(unit_kernel_done());
             for (int j = 0; j < inner; ++j) {
                 SPTB_TRY(forward_spec(QH, nullptr));                // Qhat = F(p)
                 SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
-                SPTB_TRY(grid<2>(OpTvGradNorm{Pd, us, X, Y}, sums2));
+                SPTB_TRY(grid<2>(OpTvGradNorm<C>{G, us, X, Y}, sums2));
                 k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
                 SPTB_TRY(unit_kernel_done());
-                SPTB_TRY(spec<true>(RHd, QH, RH, sums));             // rho_a -= alpha A p
-                SPTB_TRY(grid<0>(OpTvStep{Ud, rx, ry, Pd, us, X, Y}, nullptr));
+                SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));     // rho_a -= alpha A p (in place)
+                SPTB_TRY(grid<0>(OpTvStep<C>{U, rx, ry, G, us, X, Y}, nullptr));
                 SPTB_TRY(adjoint_grid(RH, true));
-                SPTB_TRY(grid<2>(OpTvS<R, 1>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, sums2));
+                SPTB_TRY(grid<2>(OpTvS<R, 1, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, sums2));
                 k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 1);
                 SPTB_TRY(unit_kernel_done());
-                SPTB_TRY(grid<2>(OpTvS<R, 2>{W, Pd, rx, ry, deapo(), invP, us, X, Y}, nullptr));
+                SPTB_TRY(grid<2>(OpTvS<R, 2, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, nullptr));
             }
-            if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
-            // shrink + Bregman; W = deapo u; non-finite u
-            SPTB_TRY(grid<1>(OpTvShrink<R>{Ud, dx, dy, bx, by, W, deapo(), us, X, Y}, sums3));
+            if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<C>{U, us}, nullptr));
+            // shrink + Bregman + the next stacked target; W = deapo u; non-finite u
+            SPTB_TRY(grid<1>(OpTvShrink<R, C>{U, rx, ry, bx, by, W, deapo(), us, X, Y}, sums3));
             // residual b - A u (reused as the next outer rho_a: same u)
             SPTB_TRY(forward_spec(RH, BH));
             SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
             k_tv_check<<<1, 64, 0, st>>>(us, sums, sums3, p->P, it, B, hist, cfg.tol);
-            SPTB_TRY(unit_kernel_done());
-            const long long n = (long long)B * p->N;
-            k_convert<C, D2><<<(int)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, st>>>(RH, RHd, n);
             SPTB_TRY(unit_kernel_done());
         }
         k_tv_finish<<<1, 64, 0, st>>>(us, B);

@@ -13,8 +13,9 @@ plan = ops.plan
 g = torch.Generator(device="cuda").manual_seed(0)
 sino = torch.randn(64, T, n_p, device="cuda", generator=g)
 res = {}
-for mode in ("0", "1"):
-    os.environ["SPTB_SPMM_ROWS"] = mode
+for mode in ("direct", "tileout", "rows"):
+    os.environ["SPTB_SPMM_ROWS"] = "1" if mode == "rows" else "0"
+    os.environ["SPTB_SPMM_TILE_OUT"] = "1" if mode == "tileout" else "0"
     _lib.lib.sptb_reload_switches()
     ms, uin = C.c_double(), C.c_int64()
     _lib.check(_lib.lib.sptb_time_spmm(plan.h, 2, 32, 30, C.byref(ms), C.byref(uin)))
@@ -28,6 +29,6 @@ for mode in ("0", "1"):
         ops.iradon(sino)
     e1.record(); torch.cuda.synchronize()
     res[mode] = rec
-    print(f"SPMM_ROWS={mode}: S {ms.value:.4f} ms {byt / ms.value / 1e6:.0f} GB/s; gridrec step {e0.elapsed_time(e1)/10:.3f} ms", flush=True)
-d = (res["0"] - res["1"]).norm() / res["1"].norm()
-print("rel diff seg vs rows:", float(d))
+    print(f"{mode}: S {ms.value:.4f} ms {byt / ms.value / 1e6:.0f} GB/s; gridrec step {e0.elapsed_time(e1)/10:.3f} ms", flush=True)
+for m in ("direct", "tileout"):
+    print(f"rel diff {m} vs rows:", float((res[m] - res["rows"]).norm() / res["rows"].norm()))

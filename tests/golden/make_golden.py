@@ -211,6 +211,37 @@ def threshold_case(sp):
     return out
 
 
+def cli_case(sp):
+    """The reference CLI end to end (cli.py:111-161): phantom sinogram volume
+    (odd slice count, noise) -> recon fbp / sirt-4 / cgls-3 (+ metrics JSON)
+    and an intensity volume of the same stack -> recon fbp."""
+    import json
+    import tempfile
+    from sptomo.cli import main as cli
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        sino = os.path.join(td, "sino.spt")
+        assert cli(["phantom", "--size", "32", "--slices", "3", "--angles", "20", "--noise", "0.01",
+                    "--seed", "4", "--out", sino]) == 0
+        out["sino_bytes"] = np.frombuffer(open(sino, "rb").read(), dtype=np.uint8)
+        for algo, iters in (("fbp", 1), ("sirt", 4), ("cgls", 3)):
+            rec = os.path.join(td, f"rec_{algo}.spt")
+            met = os.path.join(td, f"met_{algo}.json")
+            assert cli(["recon", "--in", sino, "--out", rec, "--algo", algo, "--iters", str(iters),
+                        "--metrics-out", met]) == 0
+            out[f"rec_{algo}"] = sp.read_volume(rec).data
+            out[f"hist_{algo}"] = np.asarray(json.load(open(met))[0]["residual_history"])
+        v = sp.read_volume(sino)
+        inten = os.path.join(td, "int.spt")
+        sp.write_volume(inten, sp.io.KIND_INTENSITY, sp.io.simulate_intensity(v.data, 1.0),
+                        center=v.center, angles=v.angles)
+        out["int_bytes"] = np.frombuffer(open(inten, "rb").read(), dtype=np.uint8)
+        rec = os.path.join(td, "rec_int.spt")
+        assert cli(["recon", "--in", inten, "--out", rec, "--algo", "fbp"]) == 0
+        out["rec_int_fbp"] = sp.read_volume(rec).data
+    return out
+
+
 def pipeline_case(sp):
     """run_pipeline on an odd 5-slice stack (test_pipeline.py:131-136)."""
     geom = sp.ScanGeometry(n_p=32, n_theta=12, n_z=5)
@@ -272,6 +303,10 @@ def main():
     np.savez_compressed(os.path.join(OUT, "threshold_g32.npz"), **threshold_case(sp))
     print("wrote threshold")
     if "--threshold-only" in sys.argv:
+        return
+    np.savez_compressed(os.path.join(OUT, "cli_g32.npz"), **cli_case(sp))
+    print("wrote cli")
+    if "--cli-only" in sys.argv:
         return
     for name, gkw, kkw in GEOMS:
         d = operators_case(sp, name, gkw, kkw)

@@ -203,9 +203,12 @@ def test_precondition_matches_reference(sb):
         assert rel(sb.precondition_apply(pre, d["s"]), d[f"pre_{kind}_s"]) <= 1e-12
         out = sb.precondition_apply(pre, d["sc"])
         assert np.iscomplexobj(out) and rel(out, d[f"pre_{kind}_sc"]) <= 1e-12
-        assert rel(sb.precondition_apply(pre, d["s"], ops), d[f"pre_{kind}_s"]) <= 1e-12
+        # through a complex64 bundle: that plan's precision
+        assert rel(sb.precondition_apply(pre, d["s"], ops), d[f"pre_{kind}_s"]) <= 1e-6
     ops_h = sb.build_operators(geom, filter_kind="hamming")
-    assert rel(ops_h.precondition(d["s"]), d["ops_hamming_precondition_s"]) <= 1e-12
+    assert rel(ops_h.precondition(d["s"]), d["ops_hamming_precondition_s"]) <= 1e-6
+    ops_h64 = sb.build_operators(geom, filter_kind="hamming", precision="complex128")
+    assert rel(ops_h64.precondition(d["s"]), d["ops_hamming_precondition_s"]) <= 1e-12
     pre = sb.Preconditioner(weights=d["wfull"])
     assert rel(sb.precondition_apply(pre, d["sc"]), d["pre_full_sc"]) <= 1e-12
     hpre = ops.preconditioner("hamming")
