@@ -41,7 +41,6 @@ void reload_switches() {
     s.fft1_perm = env_on("SPTB_FFT1_PERM");
     s.sirt_unfused = env_on("SPTB_SIRT_UNFUSED");
     s.spmm_rows = env_on("SPTB_SPMM_ROWS");
-    s.spmm_tile_out = env_on("SPTB_SPMM_TILE_OUT");
     s.pipe_chunks = std::max(0, env_int("SPTB_PIPE_CHUNKS"));
     g_switches = s;
     g_switches_read = true;

@@ -88,20 +88,16 @@ struct Acc {
 // output tile: row r, 16-byte slot cp (columns 2cp, 2cp+1) at r*16 + (cp ^ (r & 7))
 __device__ __forceinline__ int oslot(int r, int cp) { return r * (SEG_BB / 2) + (cp ^ (r & 7)); }
 
-template <bool DIRECT>
 __global__ void __launch_bounds__(SEG_THREADS, 4)
 k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const float2* __restrict__ val,
            const float2* __restrict__ x, float2* __restrict__ y, long long M,
            const int4* __restrict__ tiles, const unsigned long long* __restrict__ pairs,
            const int* __restrict__ longs, int n_long) {
     extern __shared__ __align__(16) unsigned char smem[];
-    // DIRECT: finished rows go straight to Y (8-byte stores per column; L2
-    // merges the sectors) and shared memory holds only the tile's metadata
-    constexpr int OB = DIRECT ? 0 : SEG_OUT_BYTES;
-    float4* out = reinterpret_cast<float4*>(smem + (DIRECT ? SEG_W * 12 + (SEG_TR / 2 + 1) * 8 : 0));
-    int* s_col = reinterpret_cast<int*>(smem + OB);
-    float2* s_val = reinterpret_cast<float2*>(smem + OB + SEG_W * 4);
-    unsigned long long* s_pair = reinterpret_cast<unsigned long long*>(smem + OB + SEG_W * 12);
+    float4* out = reinterpret_cast<float4*>(smem);
+    int* s_col = reinterpret_cast<int*>(smem + SEG_OUT_BYTES);
+    float2* s_val = reinterpret_cast<float2*>(smem + SEG_OUT_BYTES + SEG_W * 4);
+    unsigned long long* s_pair = reinterpret_cast<unsigned long long*>(smem + SEG_OUT_BYTES + SEG_W * 12);
 
     const int tid = threadIdx.x, h = tid >> 4, l = tid & 15;
     const float4* xl = reinterpret_cast<const float4*>(x) + l;  // lane's 16 bytes of a 256-byte row
@@ -188,18 +184,8 @@ k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const f
             for (; k + 8 <= nmin; k += 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
             for (; k < nmax; k += 8) acc.pred<8>(s_col, s_val, xl, mybeg + k, mylen - k);
         }
-        if (has) {
-            if (DIRECT) {
-                const float4 v = acc.result();
-                float2* yb = y + (size_t)(2 * l) * M + r0 + my;
-                yb[0] = make_float2(v.x, v.y);
-                yb[M] = make_float2(v.z, v.w);
-            } else {
-                out[oslot(my, l)] = acc.result();
-            }
-        }
+        if (has) out[oslot(my, l)] = acc.result();
     }
-    if (DIRECT) return;
     __syncthreads();
 
     // ---- epilogue: Y[b][r0 + r]; warp w takes 16-byte column slots cp,
@@ -293,19 +279,9 @@ int launch_spmm_seg(sptb_plan* p, const DevCSR& A, const void* vals, const void*
     const SSeg& s = p->sseg;
     const unsigned grid = (unsigned)(s.n_long + s.n_tiles);
     if (grid == 0) return SPTB_OK;
-    if (switches().spmm_tile_out) {
-        SPTB_CUDA(set_smem_once((const void*)k_spmm_seg<false>, SEG_SMEM, -1));
-        k_spmm_seg<false><<<grid, SEG_THREADS, SEG_SMEM, st>>>(A.row_ptr, A.col, (const float2*)vals,
-                                                             (const float2*)x, (float2*)y, p->M, s.tiles,
-                                                             s.pairs, s.longs, s.n_long);
-    } else {
-        // the long-row CTAs still reduce through a small shared buffer
-        constexpr int sm = SEG_W * 12 + (SEG_TR / 2 + 1) * 8 + SEG_HALVES * (SEG_BB / 2) * 16;
-        SPTB_CUDA(set_smem_once((const void*)k_spmm_seg<true>, sm, -1));
-        k_spmm_seg<true><<<grid, SEG_THREADS, sm, st>>>(A.row_ptr, A.col, (const float2*)vals,
-                                                      (const float2*)x, (float2*)y, p->M, s.tiles, s.pairs,
-                                                      s.longs, s.n_long);
-    }
+    SPTB_CUDA(set_smem_once((const void*)k_spmm_seg, SEG_SMEM, -1));
+    k_spmm_seg<<<grid, SEG_THREADS, SEG_SMEM, st>>>(A.row_ptr, A.col, (const float2*)vals, (const float2*)x,
+                                                  (float2*)y, p->M, s.tiles, s.pairs, s.longs, s.n_long);
     SPTB_LAUNCHED();
     return SPTB_OK;
 }

@@ -13,9 +13,8 @@ plan = ops.plan
 g = torch.Generator(device="cuda").manual_seed(0)
 sino = torch.randn(64, T, n_p, device="cuda", generator=g)
 res = {}
-for mode in ("direct", "tileout", "rows"):
+for mode in ("pairs", "rows"):
     os.environ["SPTB_SPMM_ROWS"] = "1" if mode == "rows" else "0"
-    os.environ["SPTB_SPMM_TILE_OUT"] = "1" if mode == "tileout" else "0"
     _lib.lib.sptb_reload_switches()
     ms, uin = C.c_double(), C.c_int64()
     _lib.check(_lib.lib.sptb_time_spmm(plan.h, 2, 32, 30, C.byref(ms), C.byref(uin)))
@@ -30,5 +29,5 @@ for mode in ("direct", "tileout", "rows"):
     e1.record(); torch.cuda.synchronize()
     res[mode] = rec
     print(f"{mode}: S {ms.value:.4f} ms {byt / ms.value / 1e6:.0f} GB/s; gridrec step {e0.elapsed_time(e1)/10:.3f} ms", flush=True)
-for m in ("direct", "tileout"):
+for m in ("pairs",):
     print(f"rel diff {m} vs rows:", float((res[m] - res["rows"]).norm() / res["rows"].norm()))
