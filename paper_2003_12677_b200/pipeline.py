@@ -167,6 +167,7 @@ def _device_solver(ops, cfg):
         iters = [r.iterations_run for r in reps]
         conv = [r.converged for r in reps]
         return rec, final, iters, conv, stat
+    run.batch_units = ops.plan.max_batch
     return run
 
 
@@ -205,9 +206,21 @@ def run_pipeline(stack: SinogramStack, cfg, workers: int = 1, ops=None, max_per_
         solve_fn = solver or _device_solver(ops, cfg)
         n_z = stack.n_z
         n_units = (n_z + 1) // 2
-        direct = out is not None and solver is None and isinstance(stack.data, np.ndarray)
-        if direct:  # results straight into the caller's (e.g. memory-mapped) volume
-            rec, final, iters, conv, stat = solve_fn(stack.data, out=out)
+        direct = solver is None and isinstance(stack.data, np.ndarray) and _cuda_ok()
+        if direct:
+            # host stack on a GPU: chunked, copies overlapped with the solve,
+            # results straight into ``out`` (e.g. a memory-mapped volume) or a
+            # new float64 stack
+            import torch
+            dev = torch.device("cuda", torch.cuda.current_device())
+            f64 = ops.plan.precision == _f64_precision()
+            dt = torch.float64 if f64 else torch.float32
+            Y, X = geom.grid_shape
+            dst = out if out is not None else np.empty((n_z, Y, X), dtype=np.float64)
+            chunk = 2 * _stream_units(solve_fn)
+            final, iters, conv, stat = _streamed(stack.data, 0, n_z, solve_fn, dev, dt, chunk,
+                                                 _host_sink(dst, dev, dt, chunk, (Y, X)))
+            rec = dst
         else:
             rec, final, iters, conv, stat = solve_fn(stack.data)
         bad = [u for u in range(n_units) if stat[u] != 0]
@@ -227,6 +240,8 @@ def run_pipeline(stack: SinogramStack, cfg, workers: int = 1, ops=None, max_per_
             if not direct:
                 out[...] = np.asarray(rec.cpu().numpy() if hasattr(rec, "cpu") else rec)
             vol = out
+        elif direct:
+            vol = rec
         else:
             vol = np.asarray(rec.cpu().numpy() if hasattr(rec, "cpu") else rec, dtype=np.float64)
         from .solvers import SolverReport
@@ -241,6 +256,19 @@ def run_pipeline(stack: SinogramStack, cfg, workers: int = 1, ops=None, max_per_
     solve_fn = solver or _device_solver(ops, cfg)
     f64 = ops is not None and ops.plan.precision == _f64_precision()
     return _run_distributed(stack, cfg, solve_fn, dist, t0, workers, max_per_pass, f64, out)
+
+
+def _cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def _stream_units(solve_fn):
+    """Units (complex pairs) per streamed chunk: the solver's launch batch."""
+    return max(1, int(getattr(solve_fn, "batch_units", 32)))
 
 
 def _f64_precision():
@@ -302,6 +330,75 @@ def _h2d(host, lo, hi, dtype, dev):
     return t.clone()
 
 
+def _streamed(host, lo, hi, solve_fn, dev, dt, chunk, sink):
+    """Solve slices [lo, hi) of a host stack chunk by chunk with the copies
+    off the critical path: the next chunk's host -> pinned -> device copy and
+    the previous chunk's device -> host store run on side streams from two
+    helper threads while the current chunk is solved (the ctypes call
+    releases the GIL).  ``sink(a, b, rec)`` receives each chunk's device
+    result on the helper thread after its solve.  Returns the per-unit
+    (final, iters, conv, stat) lists in slice order."""
+    import concurrent.futures as cf
+    import torch
+    np_dt = np.float64 if dt == torch.float64 else np.float32
+    bounds = [(a, min(a + chunk, hi)) for a in range(lo, hi, chunk)]
+    T, P = host.shape[1:]
+    pins = [torch.empty((min(chunk, hi - lo), T, P), dtype=dt, pin_memory=True) for _ in range(2)]
+    h2d = torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+
+    def load(i):
+        a, b = bounds[i]
+        buf = pins[i % 2][: b - a]
+        np.copyto(buf.numpy(), np.asarray(host[a:b]), casting="same_kind")
+        with torch.cuda.stream(h2d):
+            d = buf.to(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        return d, ev
+
+    meta = ([], [], [], [])
+    stores = []
+    with cf.ThreadPoolExecutor(1) as ex_in, cf.ThreadPoolExecutor(1) as ex_out:
+        nxt = ex_in.submit(load, 0)
+        for i, (a, b) in enumerate(bounds):
+            d, ev = nxt.result()
+            if i + 1 < len(bounds):
+                nxt = ex_in.submit(load, i + 1)
+            cur.wait_event(ev)
+            rec, final, iters, conv, stat = solve_fn(d)
+            for acc, v in zip(meta, (final, iters, conv, stat)):
+                acc.extend(v)
+            done = torch.cuda.Event()
+            done.record(cur)
+            if len(stores) >= 2:
+                stores[-2].result()  # bound the results in flight
+            stores.append(ex_out.submit(sink, a, b, rec, done))
+        for f in stores:
+            f.result()
+    return meta
+
+
+def _host_sink(out, dev, dt, chunk, T_shape):
+    """sink for _streamed: device result -> pinned -> host volume ``out``."""
+    import torch
+    d2h = torch.cuda.Stream(dev)
+    pins = [torch.empty((chunk,) + tuple(T_shape), dtype=dt, pin_memory=True) for _ in range(3)]
+    count = [0]
+
+    def sink(a, b, rec, done):
+        buf = pins[count[0] % 3][: b - a]
+        count[0] += 1
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            buf.copy_(rec, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+        ev.synchronize()
+        out[a:b] = buf.numpy()
+    return sink
+
+
 def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64=False, out=None):
     import torch
     import torch.distributed as tdist
@@ -327,7 +424,12 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64
     lo, hi = spans[rank]
 
     # ---- input: own range over this rank's PCIe link, or rank 0 -> ranks over NCCL
-    if local_in:
+    streamed = local_in and dev.type == "cuda" and isinstance(stack.data, np.ndarray)
+    if streamed:
+        # copies overlapped with the solve, chunk by chunk (results either
+        # straight to ``out`` or into this rank's device range for the gather)
+        mine = None
+    elif local_in:
         mine = _h2d(stack.data, lo, hi, dt, dev)
     else:
         mine = torch.empty((hi - lo, T, P), dtype=dt, device=dev)
@@ -348,7 +450,21 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64
 
     # ---- solve (no collective inside)
     ul = ranges[rank][1]
-    if ul > 0:
+    if ul > 0 and streamed:
+        chunk = 2 * _stream_units(solve_fn)
+        if local_out:
+            sink = _host_sink(out, dev, dt, chunk, (Y, X))
+            rec = None
+        else:
+            rec = torch.empty((hi - lo, Y, X), dtype=dt, device=dev)
+
+            def sink(a, b, r, done, _rec=rec):
+                torch.cuda.current_stream(dev).wait_event(done)
+                _rec[a - lo:b - lo].copy_(r)
+        final, iters, conv, stat = _streamed(stack.data, lo, hi, solve_fn, dev, dt, chunk, sink)
+        if rec is None:
+            rec = torch.empty((0, Y, X), dtype=dt, device=dev)
+    elif ul > 0:
         rec, final, iters, conv, stat = solve_fn(mine)
         rec = torch.as_tensor(rec, device=dev).to(dt)
     else:
@@ -359,7 +475,7 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64
 
     # ---- output: own range device -> host, or ranks -> rank 0 over NCCL
     vol = None
-    if local_out:
+    if local_out and not streamed:
         if hi > lo:
             out[lo:hi] = rec.cpu().numpy()
     ops_ = []
