@@ -808,6 +808,8 @@ struct OpTvShrink {
 // chan_scale(alpha, Qhat) through the mirror mix (stepped units only); then the
 // A, C partial sums of the (updated) Rhat.  RV = storage of Rhat; rf = optional
 // plan-precision copy of Rhat for the next SpMM.
+constexpr int SPEC_Q = 4;  // work items per detector row in k_spec
+
 template <typename R, typename RV, bool UPDATE>
 __global__ void __launch_bounds__(RT)
 k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
@@ -825,13 +827,16 @@ k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
         ap = 0.5 * (us[b].alpha[0] + us[b].alpha[1]);
         am = 0.5 * (us[b].alpha[0] - us[b].alpha[1]);
     }
-    // blocks walk whole detector rows t; inside a row (jh, b) in 32-bit math
-    // (B is a power of two: the divide is a shift)
+    // work item = (detector row t, quarter q of its bins jh): 4T items for a
+    // grid of 4T blocks (whole rows per block left a 1.3-wave tail: T = 1536
+    // rows on 1184 blocks); inside an item (jh, b) in 32-bit math (B is a
+    // power of two: the divide is a shift)
     (void)total;
     (void)stride;
-    const int per_row = H * B;
-    for (int t = blockIdx.x; t < T; t += gridDim.x)
-    for (int e = threadIdx.x; e < per_row; e += RT) {
+    for (int item = blockIdx.x; item < T * SPEC_Q; item += gridDim.x) {
+    const int t = item / SPEC_Q, q = item - t * SPEC_Q;
+    const int e_beg = (H * q / SPEC_Q) * B, e_end = (H * (q + 1) / SPEC_Q) * B;
+    for (int e = e_beg + threadIdx.x; e < e_end; e += RT) {
         const int jh = e / B;
         const int j1 = jh, j2 = (P - jh) % P;
         if (j1 > j2 && j2 != 0) continue;  // odd P: each pair once
@@ -862,6 +867,7 @@ k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
             a += wt * (r1.x * r1.x + r1.y * r1.y + r2.x * r2.x + r2.y * r2.y);
             c += 2.0 * wt * (r1.x * r2.x - r1.y * r2.y);
         }
+    }
     }
     // reduce threads sharing b (tid = b + B*k), fixed order
     __shared__ double sa[RT], sc[RT];
@@ -1300,7 +1306,7 @@ struct Solver {
             for (D2** q : {&Rg, &SHg, &Qg, &Hg, &Vg}) SPTB_TRY(alloc((void**)q, gd));
         }
         nblk_grid = std::max(1, 1184 / B);
-        nblk_spec = 1184;
+        nblk_spec = p->T * SPEC_Q;
         const size_t np = (size_t)std::max(nblk_grid, nblk_spec) * B * 4;
         SPTB_TRY(alloc((void**)&part, sizeof(double) * np));
         SPTB_TRY(alloc((void**)&sums, sizeof(double) * B * 4));
