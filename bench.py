@@ -315,7 +315,7 @@ def run_ours(a):
                       "frac_of_peak": alg / msl.value / 1e6 / peak}
     traffic = _traffic_from_profiles()
     s = spmm["S_filtered"]
-    roofline = {"kernel": "sptb::k_spmm (S diag(w), gridrec)", "bound": "hbm",
+    roofline = {"kernel": "sptb::k_spmm_seg (S diag(w), gridrec)", "bound": "hbm",
                 "achieved": s["gbs"], "peak": peak, "unit": "GB/s", "frac": s["gbs"] / peak,
                 "traffic": traffic.get("S"), "peak_source": peak_src,
                 "bytes_model": "12*nnz + 4*(rows+1) + 8*B*(U_in + rows) per launch"}

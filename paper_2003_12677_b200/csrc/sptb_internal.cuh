@@ -140,7 +140,7 @@ struct Switches {
     bool fft2_no_persist = false, fft2_no_bulk = false;
     bool fft1_stockham = false, fft1_no_bulk = false, fft1_r16_inv = false;
     bool fft1_inv_gather = false, fft1_fwd_rows = false, fft1_perm = false;
-    bool sirt_unfused = false, spmm_rows = false;
+    bool sirt_unfused = false, spmm_rows = false, no_graph = false;
     int sh_grid = 0;       // S^H launch grid override (0: default)
     int pipe_chunks = 0;   // host pipeline chunks per call (0: default)
 };
@@ -215,6 +215,8 @@ struct sptb_plan {
     // (cudaMalloc/cudaFree per solve stalled the stream and varied by ms)
     std::vector<std::pair<size_t, void*>> pool;
     int* solver_pinned = nullptr;        // lagged early-exit counters
+    cudaStream_t solver_stream = nullptr;  // solves run here (capturable: not the legacy stream)
+    cudaEvent_t solver_join[2] = {};
     cudaEvent_t solver_ev[4] = {};
 };
 

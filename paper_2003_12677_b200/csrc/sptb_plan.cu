@@ -41,6 +41,7 @@ void reload_switches() {
     s.fft1_perm = env_on("SPTB_FFT1_PERM");
     s.sirt_unfused = env_on("SPTB_SIRT_UNFUSED");
     s.spmm_rows = env_on("SPTB_SPMM_ROWS");
+    s.no_graph = env_on("SPTB_NO_GRAPH");
     s.pipe_chunks = std::max(0, env_int("SPTB_PIPE_CHUNKS"));
     g_switches = s;
     g_switches_read = true;
@@ -471,6 +472,9 @@ int sptb_plan_destroy(sptb_plan* p) {
     if (p->solver_pinned) cudaFreeHost(p->solver_pinned);
     for (auto& e : p->solver_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : p->solver_join)
+        if (e) cudaEventDestroy(e);
+    if (p->solver_stream) cudaStreamDestroy(p->solver_stream);
     delete p;
     return SPTB_OK;
 }

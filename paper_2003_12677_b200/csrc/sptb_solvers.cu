@@ -176,15 +176,43 @@ __device__ __forceinline__ typename CT<R>::T rc(double x, double y) {
 // forward differences (solvers.py:308-314): last column / row zero.  V is
 // the storage type of the TV state (the plan's complex type); arithmetic is
 // fp64
+// grid point m -> (x, y) in 32-bit float-reciprocal arithmetic with a +-1
+// fix-up (exact for m < 2^24): the 64-bit m % X and m / X these stencil
+// helpers used cost ~90 instructions per element and made the TV passes
+// instruction-bound (ncu: 382 M instructions for one gradient-norm pass)
+__device__ __forceinline__ void split_m(long long m, int X, int& x, int& y) {
+    if (m >= (1LL << 24)) {  // grids beyond 4096^2: exact integer division
+        x = (int)(m % X);
+        y = (int)(m / X);
+        return;
+    }
+    const int mi = (int)m;
+    int q = __float2int_rz(__int2float_rn(mi) * __frcp_rn((float)X));
+    int r = mi - q * X;
+    if (r < 0) {
+        q -= 1;
+        r += X;
+    } else if (r >= X) {
+        q += 1;
+        r -= X;
+    }
+    x = r;
+    y = q;
+}
+
 template <typename V>
 __device__ __forceinline__ D2 grad_x(const V* v, size_t i, long long m, int X) {
-    if ((int)(m % X) == X - 1) return make_double2(0, 0);
+    int x, y;
+    split_m(m, X, x, y);
+    if (x == X - 1) return make_double2(0, 0);
     const D2 a = d2(v[i]), b = d2(v[i + 1]);
     return make_double2(b.x - a.x, b.y - a.y);
 }
 template <typename V>
 __device__ __forceinline__ D2 grad_y(const V* v, size_t i, long long m, int X, int Y) {
-    if ((int)(m / X) == Y - 1) return make_double2(0, 0);
+    int x, y;
+    split_m(m, X, x, y);
+    if (y == Y - 1) return make_double2(0, 0);
     const D2 a = d2(v[i]), b = d2(v[i + X]);
     return make_double2(b.x - a.x, b.y - a.y);
 }
@@ -192,7 +220,8 @@ __device__ __forceinline__ D2 grad_y(const V* v, size_t i, long long m, int X, i
 template <typename V>
 __device__ __forceinline__ D2 grad_t(const V* vx, const V* vy, size_t i, long long m, int X, int Y) {
     // div2d(vx,vy)[y][x] = vx[x] (x<X-1) - vx[x-1] (x>0) + same along y; return its negative
-    const int x = (int)(m % X), y = (int)(m / X);
+    int x, y;
+    split_m(m, X, x, y);
     double re = 0, im = 0;
     if (x < X - 1) { re += (double)vx[i].x; im += (double)vx[i].y; }
     if (x > 0) { re -= (double)vx[i - 1].x; im -= (double)vx[i - 1].y; }
@@ -206,6 +235,62 @@ __device__ __forceinline__ V tv_store(double x, double y) {
     v.x = x;
     v.y = y;
     return v;
+}
+
+// Raw stencil neighbours, loaded in an op's load() phase and differenced in
+// apply(): the loads of all of a thread's elements are then in flight
+// together (differencing inside load() serialised each element's loads
+// behind the previous element's fp64 conversions: ncu long-scoreboard).
+template <typename V>
+struct Fwd {  // centre, right (x+1), down (y+1); forward differences
+    V c, r, d;
+    bool hr, hd;
+    __device__ __forceinline__ D2 gx() const {
+        return hr ? make_double2((double)r.x - (double)c.x, (double)r.y - (double)c.y) : make_double2(0, 0);
+    }
+    __device__ __forceinline__ D2 gy() const {
+        return hd ? make_double2((double)d.x - (double)c.x, (double)d.y - (double)c.y) : make_double2(0, 0);
+    }
+};
+template <typename V>
+__device__ __forceinline__ Fwd<V> load_fwd(const V* v, size_t i, long long m, int X, int Y) {
+    int x, y;
+    split_m(m, X, x, y);
+    Fwd<V> f;
+    f.hr = x < X - 1;
+    f.hd = y < Y - 1;
+    f.c = v[i];
+    f.r = v[f.hr ? i + 1 : i];
+    f.d = v[f.hd ? i + X : i];
+    return f;
+}
+template <typename V>
+struct Bwd {  // grad^T = -div: vx at x and x-1, vy at y and y-1
+    V xc, xl, yc, yu;
+    bool hxc, hxl, hyc, hyu;
+    __device__ __forceinline__ D2 gt() const {
+        double re = 0, im = 0;
+        if (hxc) { re += (double)xc.x; im += (double)xc.y; }
+        if (hxl) { re -= (double)xl.x; im -= (double)xl.y; }
+        if (hyc) { re += (double)yc.x; im += (double)yc.y; }
+        if (hyu) { re -= (double)yu.x; im -= (double)yu.y; }
+        return make_double2(-re, -im);
+    }
+};
+template <typename V>
+__device__ __forceinline__ Bwd<V> load_bwd(const V* vx, const V* vy, size_t i, long long m, int X, int Y) {
+    int x, y;
+    split_m(m, X, x, y);
+    Bwd<V> b;
+    b.hxc = x < X - 1;
+    b.hxl = x > 0;
+    b.hyc = y < Y - 1;
+    b.hyu = y > 0;
+    b.xc = vx[i];
+    b.xl = vx[b.hxl ? i - 1 : i];
+    b.yc = vy[i];
+    b.yu = vy[b.hyu ? i - X : i];
+    return b;
 }
 
 // ------------------------------------------------------------------ grid ops
@@ -681,21 +766,22 @@ struct OpTvS {
     double scale;
     const Unit* us;
     int X, Y;
-    struct In { C y; D2 gt, pp; R d; };
+    struct In { C y; Bwd<V> g; V pp; R d; };
     __device__ bool enabled(int b) const { return MODE == 1 || us[b].active; }
     __device__ In load(int, size_t i, long long m) const {
         In v;
         v.y = w[i];
-        v.gt = grad_t(rx, ry, i, m, X, Y);
-        v.pp = MODE == 2 ? d2(p[i]) : D2{};
+        v.g = load_bwd(rx, ry, i, m, X, Y);
+        if (MODE == 2) v.pp = p[i];
         v.d = deapo[m];
         return v;
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         const Unit& un = us[b];
         const double d = (double)v.d;
-        const D2 s = make_double2(un.mu[0] * (v.y.x * d * scale) + un.lam[0] * v.gt.x,
-                                  un.mu[1] * (v.y.y * d * scale) + un.lam[1] * v.gt.y);
+        const D2 gt = v.g.gt();
+        const D2 s = make_double2(un.mu[0] * (v.y.x * d * scale) + un.lam[0] * gt.x,
+                                  un.mu[1] * (v.y.y * d * scale) + un.lam[1] * gt.y);
         if (MODE <= 1) {
             acc[0] += s.x * s.x;
             acc[1] += s.y * s.y;
@@ -705,7 +791,7 @@ struct OpTvS {
             w[i] = rc<R>(s.x * d, s.y * d);
         }
         if (MODE == 2) {
-            D2 pp = v.pp;
+            D2 pp = d2(v.pp);
             if (!un.inner_stop) {
                 pp.x = s.x + un.beta[0] * pp.x;
                 pp.y = s.y + un.beta[1] * pp.y;
@@ -721,14 +807,13 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     const V* p;
     const Unit* us;
     int X, Y;
-    struct In { D2 gx, gy; };
+    struct In { Fwd<V> f; };
     __device__ bool enabled(int b) const { return us[b].active; }
-    __device__ In load(int, size_t i, long long m) const {
-        return In{grad_x(p, i, m, X), grad_y(p, i, m, X, Y)};
-    }
+    __device__ In load(int, size_t i, long long m) const { return In{load_fwd(p, i, m, X, Y)}; }
     __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
-        acc[0] += v.gx.x * v.gx.x + v.gy.x * v.gy.x;
-        acc[1] += v.gx.y * v.gx.y + v.gy.y * v.gy.y;
+        const D2 gx = v.f.gx(), gy = v.f.gy();
+        acc[0] += gx.x * gx.x + gy.x * gy.x;
+        acc[1] += gx.y * gx.y + gy.y * gy.y;
     }
 };
 
@@ -739,20 +824,21 @@ struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
     const V* p;
     const Unit* us;
     int X, Y;
-    struct In { D2 pp, gx, gy, x, a, c; };
+    struct In { Fwd<V> f; V x, a, c; };
     __device__ bool enabled(int b) const { return us[b].stepped; }
     __device__ In load(int, size_t i, long long m) const {
-        return In{d2(p[i]), grad_x(p, i, m, X), grad_y(p, i, m, X, Y), d2(u[i]), d2(rx[i]), d2(ry[i])};
+        return In{load_fwd(p, i, m, X, Y), u[i], rx[i], ry[i]};
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
         const Unit& un = us[b];
-        D2 x = v.x, a = v.a, c = v.c;
-        x.x += un.alpha[0] * v.pp.x;
-        x.y += un.alpha[1] * v.pp.y;
-        a.x -= un.alpha[0] * v.gx.x;
-        a.y -= un.alpha[1] * v.gx.y;
-        c.x -= un.alpha[0] * v.gy.x;
-        c.y -= un.alpha[1] * v.gy.y;
+        const D2 pp = d2(v.f.c), gx = v.f.gx(), gy = v.f.gy();
+        D2 x = d2(v.x), a = d2(v.a), c = d2(v.c);
+        x.x += un.alpha[0] * pp.x;
+        x.y += un.alpha[1] * pp.y;
+        a.x -= un.alpha[0] * gx.x;
+        a.y -= un.alpha[1] * gx.y;
+        c.x -= un.alpha[0] * gy.x;
+        c.y -= un.alpha[1] * gy.y;
         u[i] = tv_store<V>(x.x, x.y);
         rx[i] = tv_store<V>(a.x, a.y);
         ry[i] = tv_store<V>(c.x, c.y);
@@ -773,17 +859,19 @@ struct OpTvShrink {
     const R* deapo;
     const Unit* us;
     int X, Y;
-    struct In { D2 x, gx, gy, bx, by; R d; };
+    struct In { Fwd<V> f; V bx, by; R d; };
     __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const {
-        return In{d2(u[i]), grad_x(u, i, m, X), grad_y(u, i, m, X, Y), d2(bx[i]), d2(by[i]), deapo[m]};
+        return In{load_fwd(u, i, m, X, Y), bx[i], by[i], deapo[m]};
     }
-    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
+    __device__ void apply(int b, size_t i, long long, const In& in, double (&acc)[1]) const {
         const Unit& un = us[b];
-        if (!finite2(v.x.x, v.x.y)) acc[0] += 1.0;
-        const double d = (double)v.d;
-        w[i] = rc<R>(v.x.x * d, v.x.y * d);
+        const D2 x = d2(in.f.c), gxv = in.f.gx(), gyv = in.f.gy();
+        if (!finite2(x.x, x.y)) acc[0] += 1.0;
+        const double d = (double)in.d;
+        w[i] = rc<R>(x.x * d, x.y * d);
         if (!un.active) return;
+        struct { D2 gx, gy, bx, by; } v{gxv, gyv, d2(in.bx), d2(in.by)};
         const double vx[2] = {v.gx.x + v.bx.x, v.gx.y + v.bx.y};
         const double vy[2] = {v.gy.x + v.by.x, v.gy.y + v.by.y};
         double ox[2], oy[2];
@@ -945,7 +1033,11 @@ __device__ void record_residual(Unit& un, const double* ac, int P, int it, int B
     chan_norm2(ac, P, un, n2);
     const double r0 = sqrt(n2[0]), r1 = sqrt(n2[1]);
     const double res = sqrt(n2[0] + n2[1]);
-    hist[(size_t)it * B + b] = res;
+    // the unit's own count: an active unit has run every iteration so far, and
+    // the kernel's arguments stay the same from iteration to iteration (the
+    // iteration bodies are replayed as CUDA graphs)
+    (void)it;
+    hist[(size_t)un.iters * B + b] = res;
     un.iters += 1;
     if (nonfinite) {
         un.status = ST_NONFINITE;
@@ -1250,6 +1342,47 @@ struct Solver {
     static constexpr int LAG = 2;  // the host runs up to LAG iterations ahead of the device
     cudaEvent_t ev[LAG + 1] = {};
     std::vector<std::pair<size_t, void*>> owned;
+    // iteration bodies after the first are captured once and replayed as a
+    // CUDA graph: one launch per iteration instead of 10-40 (the small
+    // per-slice scalar kernels made launch overhead dominate at config-1 size)
+    cudaGraphExec_t gexec = nullptr;
+    long long gkernels = 0;
+    bool gfail = false;
+
+    template <class F>
+    int iterate(int it, F&& body) {
+        if (it == 0 || gfail || switches().no_graph) return body();
+        if (!gexec) {
+            const long long l0 = sptb_launch_count();
+            if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                cudaGetLastError();
+                gfail = true;
+                return body();
+            }
+            const int rc = body();
+            cudaGraph_t g = nullptr;
+            const cudaError_t e = cudaStreamEndCapture(st, &g);
+            gkernels = sptb_launch_count() - l0;
+            count_launch((int)-gkernels);  // captured, not run
+            if (rc != SPTB_OK || e != cudaSuccess || !g) {
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                gfail = true;
+                return rc != SPTB_OK ? rc : body();
+            }
+            const cudaError_t ei = cudaGraphInstantiate(&gexec, g, 0);
+            cudaGraphDestroy(g);
+            if (ei != cudaSuccess) {
+                cudaGetLastError();
+                gexec = nullptr;
+                gfail = true;
+                return body();
+            }
+        }
+        SPTB_CUDA(cudaGraphLaunch(gexec, st));
+        count_launch((int)gkernels);
+        return SPTB_OK;
+    }
 
     // buffers come from / return to the plan's pool (best fit within 2x)
     int alloc(void** ptr, size_t bytes) {
@@ -1278,6 +1411,7 @@ struct Solver {
         return SPTB_OK;
     }
     ~Solver() {
+        if (gexec) cudaGraphExecDestroy(gexec);
         // stream-ordered reuse: the next solve runs on the same stream
         for (auto& kv : owned) p->pool.push_back(kv);
     }
@@ -1515,6 +1649,7 @@ struct Solver {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            SPTB_TRY(iterate(it, [&]() -> int {
             // u += alpha g ; W = deapo u ; non-finite count ; Rhat = Bhat - F(u)
             if (sirt_fused_ok()) {
                 SPTB_TRY(sirt_update_forward(cfg.nonneg));
@@ -1533,7 +1668,8 @@ struct Solver {
                 SPTB_TRY(grid<4>(OpAdjPost<R, true>{W, G, deapo(), invP}, sums3));
             }
             k_sirt_alpha<<<1, 64, 0, st>>>(us, sums3, B, cfg.bb_enabled);
-            SPTB_TRY(unit_kernel_done());
+            return unit_kernel_done();
+            }));
         }
         return SPTB_OK;
     }
@@ -1557,6 +1693,7 @@ struct Solver {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            SPTB_TRY(iterate(it, [&]() -> int {
             // q = A p  -> delta, alpha, activity
             SPTB_TRY(forward_spec(QH, nullptr));
             SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
@@ -1574,7 +1711,8 @@ struct Solver {
             // u += alpha p ; p = s + beta p ; W = deapo p_new
             SPTB_TRY(grid<1>(OpCglsTail<R>{Ud, Pd, W, deapo(), invP, us}, sums3));
             k_flag_nonfinite<<<1, 64, 0, st>>>(us, sums3, B, 1);
-            SPTB_TRY(unit_kernel_done());
+            return unit_kernel_done();
+            }));
         }
         if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
         return SPTB_OK;
@@ -1600,6 +1738,7 @@ struct Solver {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            SPTB_TRY(iterate(it, [&]() -> int {
             // v = M p ; sigma ; alpha
             SPTB_TRY(normal_apply());
             SPTB_TRY(grid<2>(OpCgsV<R>{W, SHg, Vg, deapo(), invP}, sums2));
@@ -1615,7 +1754,8 @@ struct Solver {
             k_cgs_check<<<1, 64, 0, st>>>(us, sums, sums3, sums2, p->P, it, B, hist, cfg.tol);
             SPTB_TRY(unit_kernel_done());
             // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
-            SPTB_TRY(grid<0>(OpCgsDir<R>{Rg, Hg, Qg, Pd, W, deapo(), us}, nullptr));
+            return grid<0>(OpCgsDir<R>{Rg, Hg, Qg, Pd, W, deapo(), us}, nullptr);
+            }));
         }
         if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
         return SPTB_OK;
@@ -1644,6 +1784,7 @@ struct Solver {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            SPTB_TRY(iterate(it, [&]() -> int {
             // stacked CGLS on (sqrt(mu) A; sqrt(lam) grad) u = (sqrt(mu) b; sqrt(lam)(d - b));
             // rho = (d - b) - grad u comes from the previous shrink pass (0 at u = 0)
             SPTB_TRY(adjoint_grid(RH, true));
@@ -1671,7 +1812,8 @@ struct Solver {
             SPTB_TRY(forward_spec(RH, BH));
             SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
             k_tv_check<<<1, 64, 0, st>>>(us, sums, sums3, p->P, it, B, hist, cfg.tol);
-            SPTB_TRY(unit_kernel_done());
+            return unit_kernel_done();
+            }));
         }
         k_tv_finish<<<1, 64, 0, st>>>(us, B);
         return unit_kernel_done();
@@ -1784,9 +1926,24 @@ extern "C" int sptb_solve(sptb_plan* p, const sptb_solver_config* cfg, const voi
         return fail(SPTB_ERR_ARG, "unknown algorithm");
     if (n <= 0) return SPTB_OK;
     cudaSetDevice(p->device);
-    return p->prec == SPTB_PREC_F64
-               ? solve_typed<double>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
-                                     status)
-               : solve_typed<float>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
-                                    status);
+    // the solve runs on a plan-owned stream joined to the caller's by events:
+    // a capturable stream (the iteration graphs) even when the caller uses
+    // the legacy default stream
+    if (!p->solver_stream) {
+        SPTB_CUDA(cudaStreamCreateWithFlags(&p->solver_stream, cudaStreamNonBlocking));
+        for (auto& e : p->solver_join) SPTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t caller = p->stream;
+    SPTB_CUDA(cudaEventRecord(p->solver_join[0], caller));
+    SPTB_CUDA(cudaStreamWaitEvent(p->solver_stream, p->solver_join[0], 0));
+    SPTB_TRY(sptb_plan_set_stream(p, p->solver_stream));  // also rebinds the cuFFT plans
+    const int rc = p->prec == SPTB_PREC_F64
+                       ? solve_typed<double>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
+                                             status)
+                       : solve_typed<float>(p, *cfg, sino, in_fmt, rec, out_fmt, n, hist, iters, converged,
+                                            status);
+    SPTB_TRY(sptb_plan_set_stream(p, caller));
+    SPTB_CUDA(cudaEventRecord(p->solver_join[1], p->solver_stream));
+    SPTB_CUDA(cudaStreamWaitEvent(caller, p->solver_join[1], 0));
+    return rc;
 }
