@@ -88,6 +88,66 @@ struct Acc {
 // output tile: row r, 16-byte slot cp (columns 2cp, 2cp+1) at r*16 + (cp ^ (r & 7))
 __device__ __forceinline__ int oslot(int r, int cp) { return r * (SEG_BB / 2) + (cp ^ (r & 7)); }
 
+// Rows in length order, in pairs (host-built records); warp w takes pairs
+// w, w + 8, ...: half 0 the first row of the pair, half 1 the second.  The
+// two rows of a pair almost always have the same length, so both halves run
+// the same exactly-unrolled body: K loads in flight, then K packed FMA pairs.
+__device__ __forceinline__ void seg_pairs(int np_, const unsigned long long* s_pair, const int* s_col,
+                                          const float2* s_val, const float4* xl, float4* out, int tid) {
+    const int l = tid & 15;
+    const int w = tid >> 5, h2 = (tid >> 4) & 1;
+    for (int pi = w; pi < np_; pi += SEG_THREADS / 32) {
+        const unsigned long long rec = s_pair[pi];
+        const int la = (int)((rec >> 35) & 255), lb = (int)((rec >> 43) & 255);
+        const bool has = h2 ? ((rec >> 14) & 1) : true;
+        const int my = h2 ? (int)((rec >> 7) & 127) : (int)(rec & 127);
+        const int mybeg = h2 ? (int)((rec >> 25) & 1023) : (int)((rec >> 15) & 1023);
+        const int mylen = h2 ? lb : la;
+        Acc acc;
+        acc.zero();
+        if (la == lb) {
+            int k = 0, n = la;
+            if (n > SEG_EXACT) {
+                for (; n > 16; k += 8, n -= 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
+                if (n > SEG_EXACT) {  // 11..16: two exact pieces
+                    acc.exact<8>(s_col, s_val, xl, mybeg + k);
+                    k += 8;
+                    n -= 8;
+                }
+            }
+            switch (n) {
+#define SEG_CASE(K) \
+    case K: acc.exact<K>(s_col, s_val, xl, mybeg + k); break;
+                SEG_CASE(1) SEG_CASE(2) SEG_CASE(3) SEG_CASE(4) SEG_CASE(5) SEG_CASE(6)
+                SEG_CASE(7) SEG_CASE(8) SEG_CASE(9) SEG_CASE(10)
+#undef SEG_CASE
+                default: break;
+            }
+        } else {
+            const int nmin = min(la, lb), nmax = max(la, lb);
+            int k = 0;
+            for (; k + 8 <= nmin; k += 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
+            for (; k < nmax; k += 8) acc.pred<8>(s_col, s_val, xl, mybeg + k, mylen - k);
+        }
+        if (has) out[oslot(my, l)] = acc.result();
+    }
+}
+
+// Y[b][r0 + r] from the shared output tile; warp w takes 16-byte column slots
+// cp, lanes consecutive rows (256-byte runs per column)
+__device__ __forceinline__ void seg_epilogue(const float4* out, float2* y, long long M, int r0, int nr, int tid) {
+    const int w = tid >> 5;
+    const int lane = tid & 31;
+    for (int cp = w; cp < SEG_BB / 2; cp += SEG_THREADS / 32) {
+        float2* yb = y + (size_t)(2 * cp) * M + r0;
+        for (int r = lane; r < nr; r += 32) {
+            const float4 v = out[oslot(r, cp)];
+            yb[r] = make_float2(v.x, v.y);
+            yb[r + M] = make_float2(v.z, v.w);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(SEG_THREADS, 4)
 k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const float2* __restrict__ val,
            const float2* __restrict__ x, float2* __restrict__ y, long long M,
@@ -145,63 +205,12 @@ k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const f
     for (int i = tid; i < np_; i += SEG_THREADS) s_pair[i] = __ldg(pairs + t.z + i);
     __syncthreads();
 
-    // Rows in length order, in pairs (host-built records); warp w takes pairs
-    // w, w + 8, ...: half 0 the first row of the pair, half 1 the second.  The
-    // two rows of a pair almost always have the same length, so both halves
-    // run the same exactly-unrolled body: K loads in flight, then K packed
-    // FMA pairs.
-    const int w = tid >> 5, h2 = (tid >> 4) & 1;
-    for (int pi = w; pi < np_; pi += SEG_THREADS / 32) {
-        const unsigned long long rec = s_pair[pi];
-        const int la = (int)((rec >> 35) & 255), lb = (int)((rec >> 43) & 255);
-        const bool has = h2 ? ((rec >> 14) & 1) : true;
-        const int my = h2 ? (int)((rec >> 7) & 127) : (int)(rec & 127);
-        const int mybeg = h2 ? (int)((rec >> 25) & 1023) : (int)((rec >> 15) & 1023);
-        const int mylen = h2 ? lb : la;
-        Acc acc;
-        acc.zero();
-        if (la == lb) {
-            int k = 0, n = la;
-            if (n > SEG_EXACT) {
-                for (; n > 16; k += 8, n -= 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
-                if (n > SEG_EXACT) {  // 11..16: two exact pieces
-                    acc.exact<8>(s_col, s_val, xl, mybeg + k);
-                    k += 8;
-                    n -= 8;
-                }
-            }
-            switch (n) {
-#define SEG_CASE(K) \
-    case K: acc.exact<K>(s_col, s_val, xl, mybeg + k); break;
-                SEG_CASE(1) SEG_CASE(2) SEG_CASE(3) SEG_CASE(4) SEG_CASE(5) SEG_CASE(6)
-                SEG_CASE(7) SEG_CASE(8) SEG_CASE(9) SEG_CASE(10)
-#undef SEG_CASE
-                default: break;
-            }
-        } else {
-            const int nmin = min(la, lb), nmax = max(la, lb);
-            int k = 0;
-            for (; k + 8 <= nmin; k += 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
-            for (; k < nmax; k += 8) acc.pred<8>(s_col, s_val, xl, mybeg + k, mylen - k);
-        }
-        if (has) out[oslot(my, l)] = acc.result();
-    }
+    seg_pairs(np_, s_pair, s_col, s_val, xl, out, tid);
     __syncthreads();
-
-    // ---- epilogue: Y[b][r0 + r]; warp w takes 16-byte column slots cp,
-    // lanes consecutive rows (256-byte runs per column)
-    const int lane = tid & 31;
-    for (int cp = w; cp < SEG_BB / 2; cp += SEG_THREADS / 32) {
-        float2* yb = y + (size_t)(2 * cp) * M + r0;
-        for (int r = lane; r < nr; r += 32) {
-            const float4 v = out[oslot(r, cp)];
-            yb[r] = make_float2(v.x, v.y);
-            yb[r + M] = make_float2(v.z, v.w);
-        }
-    }
+    seg_epilogue(out, y, M, r0, nr, tid);
 }
 
-// Host schedule: tiles of short rows and the list of long rows (longest first)
+// Host schedule (once per plan, from S's structure): tiles of short rows and the list of long rows (longest first)
 int build_seg(sptb_plan* p) {
     SSeg& s = p->sseg;
     if (s.built) return SPTB_OK;
