@@ -358,11 +358,14 @@ def run_ours(a):
         te = torch.tensor([h0.elapsed_time(h1) / ks], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        pcie = _pcie_roofline(sino_h, out_h, sino, out, stream)
         e2e = {"value": world * n * 1e3 / float(te.item()), "unit": UNIT,
                "ms_per_step": float(te.item()),
                "h2d_bytes_per_step": int(sino_h.numel() * 4) * world,
                "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
-               "path": "sptb_iradon(plan, pinned host sinograms -> pinned host tomograms)"}
+               "path": "sptb_iradon(plan, pinned host sinograms -> pinned host tomograms)",
+               "pcie_roofline": pcie,
+               "frac_of_pcie_bound": pcie["ms_bound"] / float(te.item())}
 
     par = None
     if rank == 0 and not a.no_parity:
@@ -562,6 +565,43 @@ def _pipeline_sirt(sb, a, world, rank, dev):
             except OSError:
                 pass
     return res
+
+
+def _pcie_roofline(sino_h, out_h, sino_d, out_d, stream):
+    """The e2e bound: this step's H2D and D2H bytes over the measured pinned
+    copy bandwidth of this box, both directions at once (they overlap in the
+    pipelined call)."""
+    import torch
+    s2 = torch.cuda.Stream()
+    for _ in range(2):
+        sino_d.copy_(sino_h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(stream)
+    sino_d.copy_(sino_h, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    out_h.copy_(out_d, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    h2d_ms, d2h_ms = e0.elapsed_time(e1), f0.elapsed_time(f1)
+    # both directions together
+    torch.cuda.synchronize()
+    e0.record(stream)
+    with torch.cuda.stream(s2):
+        out_h.copy_(out_d, non_blocking=True)
+    sino_d.copy_(sino_h, non_blocking=True)
+    e2.record(s2)
+    stream.wait_event(e2)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    both_ms = e0.elapsed_time(e1)
+    hb, db = sino_h.numel() * 4, out_h.numel() * 4
+    return {"h2d_gbs": hb / h2d_ms / 1e6, "d2h_gbs": db / d2h_ms / 1e6, "duplex_ms": both_ms,
+            "ms_bound": both_ms,
+            "note": "pinned H2D of the step's sinograms concurrent with the D2H of its tomograms"}
 
 
 def _traffic_from_profiles():
