@@ -240,17 +240,28 @@ __device__ __forceinline__ V tv_store(double x, double y) {
 // Raw stencil neighbours, loaded in an op's load() phase and differenced in
 // apply(): the loads of all of a thread's elements are then in flight
 // together (differencing inside load() serialised each element's loads
-// behind the previous element's fp64 conversions: ncu long-scoreboard).
+// behind the previous element's conversions: ncu long-scoreboard).  The TV
+// element arithmetic runs in the storage type's precision (fp32 for the
+// complex64 build, fp64 for the complex128 build); reductions accumulate in
+// fp64.  (fp64 differencing and shrink made these passes fp64-issue-bound:
+// 1.66 G instructions, "wait" stalls, for one shrink pass.)
+template <typename V> struct Sc;
+template <> struct Sc<float2> { using T = float; };
+template <> struct Sc<double2> { using T = double; };
+template <typename V>
+__device__ __forceinline__ V mk(typename Sc<V>::T x, typename Sc<V>::T y) {
+    V v;
+    v.x = x;
+    v.y = y;
+    return v;
+}
+
 template <typename V>
 struct Fwd {  // centre, right (x+1), down (y+1); forward differences
     V c, r, d;
     bool hr, hd;
-    __device__ __forceinline__ D2 gx() const {
-        return hr ? make_double2((double)r.x - (double)c.x, (double)r.y - (double)c.y) : make_double2(0, 0);
-    }
-    __device__ __forceinline__ D2 gy() const {
-        return hd ? make_double2((double)d.x - (double)c.x, (double)d.y - (double)c.y) : make_double2(0, 0);
-    }
+    __device__ __forceinline__ V gx() const { return hr ? mk<V>(r.x - c.x, r.y - c.y) : mk<V>(0, 0); }
+    __device__ __forceinline__ V gy() const { return hd ? mk<V>(d.x - c.x, d.y - c.y) : mk<V>(0, 0); }
 };
 template <typename V>
 __device__ __forceinline__ Fwd<V> load_fwd(const V* v, size_t i, long long m, int X, int Y) {
@@ -268,13 +279,13 @@ template <typename V>
 struct Bwd {  // grad^T = -div: vx at x and x-1, vy at y and y-1
     V xc, xl, yc, yu;
     bool hxc, hxl, hyc, hyu;
-    __device__ __forceinline__ D2 gt() const {
-        double re = 0, im = 0;
-        if (hxc) { re += (double)xc.x; im += (double)xc.y; }
-        if (hxl) { re -= (double)xl.x; im -= (double)xl.y; }
-        if (hyc) { re += (double)yc.x; im += (double)yc.y; }
-        if (hyu) { re -= (double)yu.x; im -= (double)yu.y; }
-        return make_double2(-re, -im);
+    __device__ __forceinline__ V gt() const {
+        typename Sc<V>::T re = 0, im = 0;
+        if (hxc) { re += xc.x; im += xc.y; }
+        if (hxl) { re -= xl.x; im -= xl.y; }
+        if (hyc) { re += yc.x; im += yc.y; }
+        if (hyu) { re -= yu.x; im -= yu.y; }
+        return mk<V>(-re, -im);
     }
 };
 template <typename V>
@@ -777,25 +788,26 @@ struct OpTvS {
         return v;
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
+        using T = typename Sc<V>::T;
         const Unit& un = us[b];
-        const double d = (double)v.d;
-        const D2 gt = v.g.gt();
-        const D2 s = make_double2(un.mu[0] * (v.y.x * d * scale) + un.lam[0] * gt.x,
-                                  un.mu[1] * (v.y.y * d * scale) + un.lam[1] * gt.y);
+        const T d = (T)v.d, ds = (T)(v.d * scale);
+        const V gt = v.g.gt();
+        const V s = mk<V>((T)un.mu[0] * ((T)v.y.x * ds) + (T)un.lam[0] * gt.x,
+                          (T)un.mu[1] * ((T)v.y.y * ds) + (T)un.lam[1] * gt.y);
         if (MODE <= 1) {
-            acc[0] += s.x * s.x;
-            acc[1] += s.y * s.y;
+            acc[0] += (double)s.x * (double)s.x;
+            acc[1] += (double)s.y * (double)s.y;
         }
         if (MODE == 0) {
-            p[i] = tv_store<V>(s.x, s.y);
+            p[i] = s;
             w[i] = rc<R>(s.x * d, s.y * d);
         }
         if (MODE == 2) {
-            D2 pp = d2(v.pp);
+            V pp = v.pp;
             if (!un.inner_stop) {
-                pp.x = s.x + un.beta[0] * pp.x;
-                pp.y = s.y + un.beta[1] * pp.y;
-                p[i] = tv_store<V>(pp.x, pp.y);
+                pp.x = s.x + (T)un.beta[0] * pp.x;
+                pp.y = s.y + (T)un.beta[1] * pp.y;
+                p[i] = pp;
             }
             w[i] = rc<R>(pp.x * d, pp.y * d);
         }
@@ -811,9 +823,9 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     __device__ bool enabled(int b) const { return us[b].active; }
     __device__ In load(int, size_t i, long long m) const { return In{load_fwd(p, i, m, X, Y)}; }
     __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
-        const D2 gx = v.f.gx(), gy = v.f.gy();
-        acc[0] += gx.x * gx.x + gy.x * gy.x;
-        acc[1] += gx.y * gx.y + gy.y * gy.y;
+        const V gx = v.f.gx(), gy = v.f.gy();
+        acc[0] += (double)(gx.x * gx.x + gy.x * gy.x);
+        acc[1] += (double)(gx.y * gx.y + gy.y * gy.y);
     }
 };
 
@@ -830,18 +842,13 @@ struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
         return In{load_fwd(p, i, m, X, Y), u[i], rx[i], ry[i]};
     }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
+        using T = typename Sc<V>::T;
         const Unit& un = us[b];
-        const D2 pp = d2(v.f.c), gx = v.f.gx(), gy = v.f.gy();
-        D2 x = d2(v.x), a = d2(v.a), c = d2(v.c);
-        x.x += un.alpha[0] * pp.x;
-        x.y += un.alpha[1] * pp.y;
-        a.x -= un.alpha[0] * gx.x;
-        a.y -= un.alpha[1] * gx.y;
-        c.x -= un.alpha[0] * gy.x;
-        c.y -= un.alpha[1] * gy.y;
-        u[i] = tv_store<V>(x.x, x.y);
-        rx[i] = tv_store<V>(a.x, a.y);
-        ry[i] = tv_store<V>(c.x, c.y);
+        const T a0 = (T)un.alpha[0], a1 = (T)un.alpha[1];
+        const V pp = v.f.c, gx = v.f.gx(), gy = v.f.gy();
+        u[i] = mk<V>(v.x.x + a0 * pp.x, v.x.y + a1 * pp.y);
+        rx[i] = mk<V>(v.a.x - a0 * gx.x, v.a.y - a1 * gx.y);
+        ry[i] = mk<V>(v.c.x - a0 * gy.x, v.c.y - a1 * gy.y);
     }
 };
 
@@ -865,29 +872,30 @@ struct OpTvShrink {
         return In{load_fwd(u, i, m, X, Y), bx[i], by[i], deapo[m]};
     }
     __device__ void apply(int b, size_t i, long long, const In& in, double (&acc)[1]) const {
+        using T = typename Sc<V>::T;
         const Unit& un = us[b];
-        const D2 x = d2(in.f.c), gxv = in.f.gx(), gyv = in.f.gy();
-        if (!finite2(x.x, x.y)) acc[0] += 1.0;
-        const double d = (double)in.d;
+        const V x = in.f.c, gx = in.f.gx(), gy = in.f.gy();
+        if (!(isfinite(x.x) && isfinite(x.y))) acc[0] += 1.0;
+        const T d = (T)in.d;
         w[i] = rc<R>(x.x * d, x.y * d);
         if (!un.active) return;
-        struct { D2 gx, gy, bx, by; } v{gxv, gyv, d2(in.bx), d2(in.by)};
-        const double vx[2] = {v.gx.x + v.bx.x, v.gx.y + v.bx.y};
-        const double vy[2] = {v.gy.x + v.by.x, v.gy.y + v.by.y};
-        double ox[2], oy[2];
+        const T vx[2] = {gx.x + in.bx.x, gx.y + in.bx.y};
+        const T vy[2] = {gy.x + in.by.x, gy.y + in.by.y};
+        T ox[2], oy[2];
+#pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const double kap = 1.0 / un.lam[c];
-            const double mag = sqrt(vx[c] * vx[c] + vy[c] * vy[c]);
-            const double f = fmax(mag - kap, 0.0) / (mag > 0 ? mag : 1.0);
+            const T kap = (T)(1.0 / un.lam[c]);
+            const T mag = sqrt(vx[c] * vx[c] + vy[c] * vy[c]);
+            const T f = (mag - kap > (T)0 ? mag - kap : (T)0) / (mag > (T)0 ? mag : (T)1);
             ox[c] = vx[c] * f;
             oy[c] = vy[c] * f;
         }
-        const D2 nbx = make_double2(v.bx.x + v.gx.x - ox[0], v.bx.y + v.gx.y - ox[1]);
-        const D2 nby = make_double2(v.by.x + v.gy.x - oy[0], v.by.y + v.gy.y - oy[1]);
-        bx[i] = tv_store<V>(nbx.x, nbx.y);
-        by[i] = tv_store<V>(nby.x, nby.y);
-        rx[i] = tv_store<V>(ox[0] - nbx.x - v.gx.x, ox[1] - nbx.y - v.gx.y);
-        ry[i] = tv_store<V>(oy[0] - nby.x - v.gy.x, oy[1] - nby.y - v.gy.y);
+        const V nbx = mk<V>(in.bx.x + gx.x - ox[0], in.bx.y + gx.y - ox[1]);
+        const V nby = mk<V>(in.by.x + gy.x - oy[0], in.by.y + gy.y - oy[1]);
+        bx[i] = nbx;
+        by[i] = nby;
+        rx[i] = mk<V>(ox[0] - nbx.x - gx.x, ox[1] - nbx.y - gx.y);
+        ry[i] = mk<V>(oy[0] - nby.x - gy.x, oy[1] - nby.y - gy.y);
     }
 };
 
