@@ -31,11 +31,26 @@ namespace {
 
 constexpr int SEG_THREADS = 256;  // 8 warps = 16 half-warps
 constexpr int SEG_HALVES = SEG_THREADS / 16;
-constexpr int SEG_TR = 128;       // rows per tile (shared output tile)
-constexpr int SEG_W = 1024;       // nonzeros per tile (staged metadata)
+#ifndef SEG_TR_
+#define SEG_TR_ 128
+#endif
+#ifndef SEG_W_
+#define SEG_W_ 1024
+#endif
+#ifndef SEG_EXACT_
+#define SEG_EXACT_ 10
+#endif
+#ifndef SEG_MINB_
+#define SEG_MINB_ 4
+#endif
+constexpr int SEG_TR = SEG_TR_;   // rows per tile (shared output tile)
+constexpr int SEG_W = SEG_W_;     // nonzeros per tile (staged metadata)
 constexpr int SEG_LONG = 128;     // longer rows: one CTA per row
-constexpr int SEG_UNR = 8;        // gathers in flight per half-warp (long rows)
-constexpr int SEG_EXACT = 10;     // row lengths with an exactly unrolled body
+#ifndef SEG_UNR_
+#define SEG_UNR_ 8
+#endif
+constexpr int SEG_UNR = SEG_UNR_;  // gathers in flight per half-warp (long rows)
+constexpr int SEG_EXACT = SEG_EXACT_;  // row lengths with an exactly unrolled body
 constexpr int SEG_BB = 32;        // complex columns (batch) of this kernel
 
 // shared memory: out tile [SEG_TR][16] float4 | cols [SEG_W] | vals [SEG_W] float2 | pair records
@@ -108,26 +123,39 @@ __device__ __forceinline__ void seg_pairs(int np_, const unsigned long long* s_p
         if (la == lb) {
             int k = 0, n = la;
             if (n > SEG_EXACT) {
-                for (; n > 16; k += 8, n -= 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
-                if (n > SEG_EXACT) {  // 11..16: two exact pieces
-                    acc.exact<8>(s_col, s_val, xl, mybeg + k);
-                    k += 8;
-                    n -= 8;
+                constexpr int CK = SEG_EXACT < 8 ? SEG_EXACT : 8;
+                for (; n > SEG_EXACT + CK; k += CK, n -= CK) acc.exact<CK>(s_col, s_val, xl, mybeg + k);
+                if (n > SEG_EXACT) {  // two exact pieces
+                    acc.exact<CK>(s_col, s_val, xl, mybeg + k);
+                    k += CK;
+                    n -= CK;
                 }
             }
             switch (n) {
 #define SEG_CASE(K) \
     case K: acc.exact<K>(s_col, s_val, xl, mybeg + k); break;
                 SEG_CASE(1) SEG_CASE(2) SEG_CASE(3) SEG_CASE(4) SEG_CASE(5) SEG_CASE(6)
-                SEG_CASE(7) SEG_CASE(8) SEG_CASE(9) SEG_CASE(10)
+#if SEG_EXACT_ >= 7
+                SEG_CASE(7)
+#endif
+#if SEG_EXACT_ >= 8
+                SEG_CASE(8)
+#endif
+#if SEG_EXACT_ >= 9
+                SEG_CASE(9)
+#endif
+#if SEG_EXACT_ >= 10
+                SEG_CASE(10)
+#endif
 #undef SEG_CASE
                 default: break;
             }
         } else {
             const int nmin = min(la, lb), nmax = max(la, lb);
             int k = 0;
-            for (; k + 8 <= nmin; k += 8) acc.exact<8>(s_col, s_val, xl, mybeg + k);
-            for (; k < nmax; k += 8) acc.pred<8>(s_col, s_val, xl, mybeg + k, mylen - k);
+            constexpr int CK = SEG_EXACT < 8 ? SEG_EXACT : 8;
+            for (; k + CK <= nmin; k += CK) acc.exact<CK>(s_col, s_val, xl, mybeg + k);
+            for (; k < nmax; k += CK) acc.pred<CK>(s_col, s_val, xl, mybeg + k, mylen - k);
         }
         if (has) out[oslot(my, l)] = acc.result();
     }
@@ -148,7 +176,7 @@ __device__ __forceinline__ void seg_epilogue(const float4* out, float2* y, long 
     }
 }
 
-__global__ void __launch_bounds__(SEG_THREADS, 4)
+__global__ void __launch_bounds__(SEG_THREADS, SEG_MINB_)
 k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const float2* __restrict__ val,
            const float2* __restrict__ x, float2* __restrict__ y, long long M,
            const int4* __restrict__ tiles, const unsigned long long* __restrict__ pairs,
