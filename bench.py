@@ -472,11 +472,7 @@ def _pipeline_sirt(sb, a, world, rank, dev):
     writes its own reconstructed slices back -- no data-path collective.  The
     timed region runs from the first H2D to the last D2H (CUDA events,
     max over ranks)."""
-    import hashlib
-    import numpy as np
-    import torch
     import torch.distributed as dist
-    from oracle import shepp_logan  # synthetic phantom only
 
     nz, iters = a.pipeline_slices, a.pipeline_iters
     geom = sb.ScanGeometry(n_p=a.n_p, n_theta=a.n_theta, n_z=nz)
@@ -488,6 +484,29 @@ def _pipeline_sirt(sb, a, world, rank, dev):
     out_path = os.path.join(base, f"sptb_bench_{tag}_vol.f32")
     ops_h = sb.build_operators(sb.ScanGeometry(n_p=a.n_p, n_theta=a.n_theta), filter_kind="hamming",
                                max_batch=32)
+    try:
+        return _pipeline_sirt_run(sb, a, world, rank, dev, nz, iters, geom, T, P, Y, X, in_path, out_path, ops_h)
+    finally:
+        if world > 1:
+            try:
+                dist.barrier()
+            except Exception:
+                pass
+        if rank == 0:
+            for pth in (in_path, out_path):
+                try:
+                    os.unlink(pth)
+                except OSError:
+                    pass
+
+
+def _pipeline_sirt_run(sb, a, world, rank, dev, nz, iters, geom, T, P, Y, X, in_path, out_path, ops_h):
+    import hashlib
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from oracle import shepp_logan  # synthetic phantom only
+
     if rank == 0:
         sino = np.memmap(in_path, dtype=np.float32, mode="w+", shape=(nz, T, P))
         np.memmap(out_path, dtype=np.float32, mode="w+", shape=(nz, Y, X)).flush()
@@ -556,14 +575,6 @@ def _pipeline_sirt(sb, a, world, rank, dev):
                "workload": f"SIRT-{iters} (hamming, BB) {nz} slices {a.n_p}^2x{a.n_theta}, 2% noise, "
                            "run_pipeline over all ranks (BASELINE configs[2]); per-rank H2D/D2H of "
                            "its own slices from/to memory-mapped volumes inside the timed region"}
-    if world > 1:
-        dist.barrier()
-    if rank == 0:
-        for pth in (in_path, out_path):
-            try:
-                os.unlink(pth)
-            except OSError:
-                pass
     return res
 
 

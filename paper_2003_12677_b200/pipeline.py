@@ -383,11 +383,12 @@ def _host_sink(out, dev, dt, chunk, T_shape):
     """sink for _streamed: device result -> pinned -> host volume ``out``."""
     import torch
     d2h = torch.cuda.Stream(dev)
-    pins = [torch.empty((chunk,) + tuple(T_shape), dtype=dt, pin_memory=True) for _ in range(3)]
+    # two buffers: _streamed keeps at most two stores in flight
+    pins = [torch.empty((chunk,) + tuple(T_shape), dtype=dt, pin_memory=True) for _ in range(2)]
     count = [0]
 
     def sink(a, b, rec, done):
-        buf = pins[count[0] % 3][: b - a]
+        buf = pins[count[0] % 2][: b - a]
         count[0] += 1
         with torch.cuda.stream(d2h):
             d2h.wait_event(done)
