@@ -347,11 +347,11 @@ def _streamed(host, lo, hi, solve_fn, dev, dt, chunk, sink):
     h2d = torch.cuda.Stream(dev)
     cur = torch.cuda.current_stream(dev)
 
-    def load(i):
+    def load(i):  # helper thread: its CUDA device must be set explicitly
         a, b = bounds[i]
         buf = pins[i % 2][: b - a]
         np.copyto(buf.numpy(), np.asarray(host[a:b]), casting="same_kind")
-        with torch.cuda.stream(h2d):
+        with torch.cuda.device(dev), torch.cuda.stream(h2d):
             d = buf.to(dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(h2d)
@@ -387,10 +387,10 @@ def _host_sink(out, dev, dt, chunk, T_shape):
     pins = [torch.empty((chunk,) + tuple(T_shape), dtype=dt, pin_memory=True) for _ in range(2)]
     count = [0]
 
-    def sink(a, b, rec, done):
+    def sink(a, b, rec, done):  # helper thread
         buf = pins[count[0] % 2][: b - a]
         count[0] += 1
-        with torch.cuda.stream(d2h):
+        with torch.cuda.device(dev), torch.cuda.stream(d2h):
             d2h.wait_event(done)
             buf.copy_(rec, non_blocking=True)
             ev = torch.cuda.Event()
@@ -459,9 +459,10 @@ def _run_distributed(stack, cfg, solve_fn, group, t0, workers, max_per_pass, f64
         else:
             rec = torch.empty((hi - lo, Y, X), dtype=dt, device=dev)
 
-            def sink(a, b, r, done, _rec=rec):
-                torch.cuda.current_stream(dev).wait_event(done)
-                _rec[a - lo:b - lo].copy_(r)
+            def sink(a, b, r, done, _rec=rec):  # helper thread
+                with torch.cuda.device(dev):
+                    torch.cuda.current_stream(dev).wait_event(done)
+                    _rec[a - lo:b - lo].copy_(r)
         final, iters, conv, stat = _streamed(stack.data, lo, hi, solve_fn, dev, dt, chunk, sink)
         if rec is None:
             rec = torch.empty((0, Y, X), dtype=dt, device=dev)
