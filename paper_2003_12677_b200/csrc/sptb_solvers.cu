@@ -765,7 +765,8 @@ struct OpCgsDir {  // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
 // ------------------------------------------------------------------ grid ops (TV)
 
 // s = mu (deapo y scale) + lam grad^T(rho)   (adj(), solvers.py:397-399)
-// MODE 0: p = s, W = deapo p, acc <s,s>;  1: acc <s,s>;  2: p = s + beta p, W = deapo p
+// MODE 0: p = s, W = deapo p, acc <s,s>;  1: acc <s,s>, W = s (in place);
+// 2: W holds s (MODE 1's): p = s + beta p, W = deapo p
 template <typename R, int MODE, typename V>
 struct OpTvS {
     static constexpr int kUnroll = TV_UNROLL;
@@ -782,7 +783,7 @@ struct OpTvS {
     __device__ In load(int, size_t i, long long m) const {
         In v;
         v.y = w[i];
-        v.g = load_bwd(rx, ry, i, m, X, Y);
+        if (MODE != 2) v.g = load_bwd(rx, ry, i, m, X, Y);
         if (MODE == 2) v.pp = p[i];
         v.d = deapo[m];
         return v;
@@ -790,26 +791,28 @@ struct OpTvS {
     __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         using T = typename Sc<V>::T;
         const Unit& un = us[b];
-        const T d = (T)v.d, ds = (T)(v.d * scale);
-        const V gt = v.g.gt();
-        const V s = mk<V>((T)un.mu[0] * ((T)v.y.x * ds) + (T)un.lam[0] * gt.x,
-                          (T)un.mu[1] * ((T)v.y.y * ds) + (T)un.lam[1] * gt.y);
-        if (MODE <= 1) {
-            acc[0] += (double)s.x * (double)s.x;
-            acc[1] += (double)s.y * (double)s.y;
-        }
-        if (MODE == 0) {
-            p[i] = s;
-            w[i] = rc<R>(s.x * d, s.y * d);
-        }
+        const T d = (T)v.d;
         if (MODE == 2) {
             V pp = v.pp;
             if (!un.inner_stop) {
-                pp.x = s.x + (T)un.beta[0] * pp.x;
-                pp.y = s.y + (T)un.beta[1] * pp.y;
+                pp.x = (T)v.y.x + (T)un.beta[0] * pp.x;
+                pp.y = (T)v.y.y + (T)un.beta[1] * pp.y;
                 p[i] = pp;
             }
             w[i] = rc<R>(pp.x * d, pp.y * d);
+            return;
+        }
+        const T ds = (T)(v.d * scale);
+        const V gt = v.g.gt();
+        const V s = mk<V>((T)un.mu[0] * ((T)v.y.x * ds) + (T)un.lam[0] * gt.x,
+                          (T)un.mu[1] * ((T)v.y.y * ds) + (T)un.lam[1] * gt.y);
+        acc[0] += (double)s.x * (double)s.x;
+        acc[1] += (double)s.y * (double)s.y;
+        if (MODE == 0) {
+            p[i] = s;
+            w[i] = rc<R>(s.x * d, s.y * d);
+        } else {
+            w[i] = rc<R>(s.x, s.y);
         }
     }
 };
