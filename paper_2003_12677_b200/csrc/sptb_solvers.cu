@@ -832,26 +832,75 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     }
 };
 
-template <typename V>
-struct OpTvStep {  // u += alpha p ; rho -= alpha grad p
+// The CGLS step fused into the beta pass (solvers.py:401-413): u += alpha p,
+// rho_new = rho - alpha grad p, and s = mu (deapo y scale) + lam grad^T(rho_new)
+// with <s,s> -- rho_new at x-1 and y-1 is recomputed from the old rho and p
+// (a 5-point stencil of p), so rho is read from one buffer and written to
+// the other (neighbours still read the old values).  W (y) becomes s.
+template <typename R, typename V>
+struct OpTvStepS {
     static constexpr int kUnroll = TV_UNROLL;
-    V *u, *rx, *ry;
-    const V* p;
+    using C = typename CT<R>::T;
+    C* w;
+    V* u;
+    const V *p, *rx, *ry;  // rho (old)
+    V *nx, *ny;            // rho (new)
+    const R* deapo;
+    double scale;
     const Unit* us;
     int X, Y;
-    struct In { Fwd<V> f; V x, a, c; };
-    __device__ bool enabled(int b) const { return us[b].stepped; }
+    struct In { C y; V pc, pr, pd, pl, pu, xc, xl, yc, yu, uu; R d; bool hr, hd, hl, hu; };
+    __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const {
-        return In{load_fwd(p, i, m, X, Y), u[i], rx[i], ry[i]};
+        int x, y;
+        split_m(m, X, x, y);
+        In v;
+        v.hr = x < X - 1;
+        v.hd = y < Y - 1;
+        v.hl = x > 0;
+        v.hu = y > 0;
+        v.y = w[i];
+        v.pc = p[i];
+        v.pr = p[v.hr ? i + 1 : i];
+        v.pd = p[v.hd ? i + X : i];
+        v.pl = p[v.hl ? i - 1 : i];
+        v.pu = p[v.hu ? i - X : i];
+        v.xc = rx[i];
+        v.xl = rx[v.hl ? i - 1 : i];
+        v.yc = ry[i];
+        v.yu = ry[v.hu ? i - X : i];
+        v.uu = u[i];
+        v.d = deapo[m];
+        return v;
     }
-    __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         using T = typename Sc<V>::T;
         const Unit& un = us[b];
-        const T a0 = (T)un.alpha[0], a1 = (T)un.alpha[1];
-        const V pp = v.f.c, gx = v.f.gx(), gy = v.f.gy();
-        u[i] = mk<V>(v.x.x + a0 * pp.x, v.x.y + a1 * pp.y);
-        rx[i] = mk<V>(v.a.x - a0 * gx.x, v.a.y - a1 * gx.y);
-        ry[i] = mk<V>(v.c.x - a0 * gy.x, v.c.y - a1 * gy.y);
+        const bool st = un.stepped;
+        const T a0 = st ? (T)un.alpha[0] : (T)0, a1 = st ? (T)un.alpha[1] : (T)0;
+        // grad p at i, and the x / y differences ending at i (grad at x-1 / y-1)
+        const V gx = v.hr ? mk<V>(v.pr.x - v.pc.x, v.pr.y - v.pc.y) : mk<V>(0, 0);
+        const V gy = v.hd ? mk<V>(v.pd.x - v.pc.x, v.pd.y - v.pc.y) : mk<V>(0, 0);
+        const V gxl = mk<V>(v.pc.x - v.pl.x, v.pc.y - v.pl.y);
+        const V gyu = mk<V>(v.pc.x - v.pu.x, v.pc.y - v.pu.y);
+        const V xc = mk<V>(v.xc.x - a0 * gx.x, v.xc.y - a1 * gx.y);
+        const V yc = mk<V>(v.yc.x - a0 * gy.x, v.yc.y - a1 * gy.y);
+        const V xl = mk<V>(v.xl.x - a0 * gxl.x, v.xl.y - a1 * gxl.y);
+        const V yu = mk<V>(v.yu.x - a0 * gyu.x, v.yu.y - a1 * gyu.y);
+        if (st) u[i] = mk<V>(v.uu.x + a0 * v.pc.x, v.uu.y + a1 * v.pc.y);
+        nx[i] = xc;
+        ny[i] = yc;
+        T re = 0, im = 0;  // -grad^T(rho_new)
+        if (v.hr) { re += xc.x; im += xc.y; }
+        if (v.hl) { re -= xl.x; im -= xl.y; }
+        if (v.hd) { re += yc.x; im += yc.y; }
+        if (v.hu) { re -= yu.x; im -= yu.y; }
+        const T ds = (T)(v.d * scale);
+        const V s = mk<V>((T)un.mu[0] * ((T)v.y.x * ds) - (T)un.lam[0] * re,
+                          (T)un.mu[1] * ((T)v.y.y * ds) - (T)un.lam[1] * im);
+        acc[0] += (double)s.x * (double)s.x;
+        acc[1] += (double)s.y * (double)s.y;
+        w[i] = rc<R>(s.x, s.y);
     }
 };
 
@@ -1345,6 +1394,7 @@ struct Solver {
     // float64 Krylov state (CGLS / TV)
     D2 *Ud = nullptr, *Pd = nullptr, *RHd = nullptr;
     C *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;  // TV: Bregman b, stacked target rho
+    C *rx2 = nullptr, *ry2 = nullptr;  // TV: the other rho buffer of the fused step
     D2 *Rg = nullptr, *SHg = nullptr, *Qg = nullptr, *Hg = nullptr, *Vg = nullptr;  // CGS
     double *part = nullptr, *sums = nullptr, *sums2 = nullptr, *sums3 = nullptr, *hist = nullptr;
     Unit* us = nullptr;
@@ -1445,7 +1495,7 @@ struct Solver {
             SPTB_TRY(alloc((void**)&G, gb));
         }
         if (algo == SPTB_ALGO_TV) {
-            for (C** q : {&bx, &by, &rx, &ry}) SPTB_TRY(alloc((void**)q, gb));
+            for (C** q : {&bx, &by, &rx, &ry, &rx2, &ry2}) SPTB_TRY(alloc((void**)q, gb));
         }
         if (algo == SPTB_ALGO_CGLS && cgs) {
             for (D2** q : {&Rg, &SHg, &Qg, &Hg, &Vg}) SPTB_TRY(alloc((void**)q, gd));
@@ -1802,6 +1852,9 @@ struct Solver {
             SPTB_TRY(grid<2>(OpTvS<R, 0, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, sums2));
             k_tv_inner_begin<<<1, 64, 0, st>>>(us, sums2, B);
             SPTB_TRY(unit_kernel_done());
+            // rho ping-pongs between (rx, ry) and (rx2, ry2) through the fused
+            // step passes; S0 reads and the shrink pass writes (rx, ry)
+            C *ra = rx, *rb = ry, *wa = rx2, *wb = ry2;
             for (int j = 0; j < inner; ++j) {
                 SPTB_TRY(forward_spec(QH, nullptr));                // Qhat = F(p)
                 SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
@@ -1809,12 +1862,14 @@ struct Solver {
                 k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
                 SPTB_TRY(unit_kernel_done());
                 SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));     // rho_a -= alpha A p (in place)
-                SPTB_TRY(grid<0>(OpTvStep<C>{U, rx, ry, G, us, X, Y}, nullptr));
                 SPTB_TRY(adjoint_grid(RH, true));
-                SPTB_TRY(grid<2>(OpTvS<R, 1, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, sums2));
+                // u += alpha p ; rho -= alpha grad p ; s ; <s,s>  (W = s)
+                SPTB_TRY(grid<2>(OpTvStepS<R, C>{W, U, G, ra, rb, wa, wb, deapo(), invP, us, X, Y}, sums2));
+                std::swap(ra, wa);
+                std::swap(rb, wb);
                 k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 1);
                 SPTB_TRY(unit_kernel_done());
-                SPTB_TRY(grid<2>(OpTvS<R, 2, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, nullptr));
+                SPTB_TRY(grid<2>(OpTvS<R, 2, C>{W, G, ra, rb, deapo(), invP, us, X, Y}, nullptr));
             }
             if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<C>{U, us}, nullptr));
             // shrink + Bregman + the next stacked target; W = deapo u; non-finite u
