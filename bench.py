@@ -443,9 +443,9 @@ def _other_solvers(sb, geom, sino_clean, a, dev, stream):
     ops_n = sb.build_operators(geom, filter_kind="none", max_batch=min(64, max(1, a.slices // 2)))
     ops_n.plan.bind_stream(stream.cuda_stream)
     out = {}
-    for algo, k1, k2 in (("cgls", 2, 7), ("tv", 1, 3)):
+    for algo, k1, k2 in (("cgls", 2, 12), ("tv", 1, 4)):
         times = {}
-        for k in (k2, k1) + (k1, k2) * 2:
+        for k in (k2, k1) + (k1, k2) * 3:
             cfg = sb.SolverConfig(algorithm=algo, max_iter=k)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

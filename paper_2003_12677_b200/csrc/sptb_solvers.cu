@@ -565,11 +565,11 @@ struct OpAbsMax {  // per-channel max |deapo*y*scale| (TV default mu, solvers.py
 
 // ------------------------------------------------------------------ grid ops (CGLS, fp64 vectors)
 
-template <typename R>
+template <typename R, typename V = D2>
 struct OpCglsInit {  // p = s = deapo*y*scale ; <s,s> ; W = deapo p
     using C = typename CT<R>::T;
     C* w;
-    D2* p;
+    V* p;
     const R* deapo;
     double scale;
     struct In { C y; R d; };
@@ -580,7 +580,7 @@ struct OpCglsInit {  // p = s = deapo*y*scale ; <s,s> ; W = deapo p
         const D2 s = make_double2(v.y.x * d * scale, v.y.y * d * scale);
         acc[0] += s.x * s.x;
         acc[1] += s.y * s.y;
-        p[i] = s;
+        p[i] = tv_store<V>(s.x, s.y);
         w[i] = rc<R>(s.x * d, s.y * d);
     }
 };
@@ -602,31 +602,31 @@ struct OpDotS {  // <s,s>, s = deapo*y*scale
     }
 };
 
-template <typename R>
+template <typename R, typename V = D2>
 struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-finite u
     using C = typename CT<R>::T;
-    D2* u;
-    D2* p;
+    V* u;
+    V* p;
     C* w;  // in: y (IFFT2 output), out: deapo * p
     const R* deapo;
     double scale;
     const Unit* us;
-    struct In { D2 x, pp; C y; R d; };
+    struct In { V x, pp; C y; R d; };
     __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const { return In{u[i], p[i], w[i], deapo[m]}; }
     __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
         const Unit& un = us[b];
-        D2 x = v.x;
-        D2 pp = v.pp;
+        D2 x = d2(v.x);
+        D2 pp = d2(v.pp);
         const double d = (double)v.d;
         if (un.stepped) {
             x.x += un.alpha[0] * pp.x;
             x.y += un.alpha[1] * pp.y;
-            u[i] = x;
+            u[i] = tv_store<V>(x.x, x.y);
             if (un.active) {
                 pp.x = v.y.x * d * scale + un.beta[0] * pp.x;
                 pp.y = v.y.y * d * scale + un.beta[1] * pp.y;
-                p[i] = pp;
+                p[i] = tv_store<V>(pp.x, pp.y);
             }
         }
         if (!finite2(x.x, x.y)) acc[0] += 1.0;
@@ -1392,7 +1392,7 @@ struct Solver {
     // plan precision
     C *U = nullptr, *G = nullptr, *W = nullptr, *BH = nullptr, *RH = nullptr, *QH = nullptr;
     // float64 Krylov state (CGLS / TV)
-    D2 *Ud = nullptr, *Pd = nullptr, *RHd = nullptr;
+    D2 *Ud = nullptr, *Pd = nullptr;  // CGS iterate and direction (fp64)
     C *bx = nullptr, *by = nullptr, *rx = nullptr, *ry = nullptr;  // TV: Bregman b, stacked target rho
     C *rx2 = nullptr, *ry2 = nullptr;  // TV: the other rho buffer of the fused step
     D2 *Rg = nullptr, *SHg = nullptr, *Qg = nullptr, *Hg = nullptr, *Vg = nullptr;  // CGS
@@ -1481,16 +1481,15 @@ struct Solver {
         st = p->stream;
         SPTB_TRY(ensure_work(p, B));
         const size_t gb = sizeof(C) * (size_t)B * p->M, sb = sizeof(C) * (size_t)B * p->N;
-        const size_t gd = sizeof(D2) * (size_t)B * p->M, sd = sizeof(D2) * (size_t)B * p->N;
+        const size_t gd = sizeof(D2) * (size_t)B * p->M;
         W = (C*)p->G0;
         SPTB_TRY(alloc((void**)&BH, sb));
         SPTB_TRY(alloc((void**)&RH, sb));
         SPTB_TRY(alloc((void**)&QH, sb));
-        if (algo == SPTB_ALGO_CGLS) {
+        if (algo == SPTB_ALGO_CGLS && cgs) {  // CGS: fp64 grid vectors
             SPTB_TRY(alloc((void**)&Ud, gd));
             SPTB_TRY(alloc((void**)&Pd, gd));
-            SPTB_TRY(alloc((void**)&RHd, sd));
-        } else {  // FBP / SIRT / TV: iterate (and TV's p) in the plan's type
+        } else {  // FBP / SIRT / CGLS / TV: iterate (and p) in the plan's type
             SPTB_TRY(alloc((void**)&U, gb));
             SPTB_TRY(alloc((void**)&G, gb));
         }
@@ -1735,19 +1734,16 @@ struct Solver {
         return SPTB_OK;
     }
 
-    int copy_bh_to_rhd() {
-        const long long n = (long long)B * p->N;
-        k_convert<C, D2><<<(int)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, st>>>(BH, RHd, n);
-        return unit_kernel_done();
-    }
 
     // ---------------------------------------------------------------- CGLS
     int run_cgls(const sptb_solver_config& cfg) {
         const double invP = 1.0 / p->P;
-        // r = b (u0 = 0); s = A^H W r; p = s; gamma = <s,s>  (solvers.py:197-203)
-        SPTB_TRY(copy_bh_to_rhd());
+        // r = b (u0 = 0); s = A^H W r; p = s; gamma = <s,s>  (solvers.py:197-203).
+        // u, p and the spectral residual are stored in the plan's type (the
+        // passes are HBM-bound), the recurrence arithmetic is fp64
+        SPTB_CUDA(cudaMemcpyAsync(RH, BH, sizeof(C) * (size_t)B * p->N, cudaMemcpyDeviceToDevice, st));
         SPTB_TRY(adjoint_grid(BH, true));
-        SPTB_TRY(grid<2>(OpCglsInit<R>{W, Pd, deapo(), invP}, sums2));
+        SPTB_TRY(grid<2>(OpCglsInit<R, C>{W, G, deapo(), invP}, sums2));
         k_cgls_init<<<1, 64, 0, st>>>(us, sums2, B);
         SPTB_TRY(unit_kernel_done());
         for (int it = 0; it < cfg.max_iter; ++it) {
@@ -1760,8 +1756,8 @@ struct Solver {
             SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
             k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, nullptr, p->P, B, 0);
             SPTB_TRY(unit_kernel_done());
-            // r -= alpha q (mirror mix, fp64) and ||r||_w ; RH = plan-precision copy
-            SPTB_TRY(spec<true>(RHd, QH, RH, sums));
+            // r -= alpha q (mirror mix, fp64 arithmetic, in place) and ||r||_w
+            SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));
             k_cgls_check<<<1, 64, 0, st>>>(us, sums, p->P, it, B, hist, cfg.tol);
             SPTB_TRY(unit_kernel_done());
             // s = A^H W r ; gamma_new ; beta
@@ -1770,12 +1766,12 @@ struct Solver {
             k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 0);
             SPTB_TRY(unit_kernel_done());
             // u += alpha p ; p = s + beta p ; W = deapo p_new
-            SPTB_TRY(grid<1>(OpCglsTail<R>{Ud, Pd, W, deapo(), invP, us}, sums3));
+            SPTB_TRY(grid<1>(OpCglsTail<R, C>{U, G, W, deapo(), invP, us}, sums3));
             k_flag_nonfinite<<<1, 64, 0, st>>>(us, sums3, B, 1);
             return unit_kernel_done();
             }));
         }
-        if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<D2>{Ud, us}, nullptr));
+        if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<C>{U, us}, nullptr));
         return SPTB_OK;
     }
 
