@@ -547,6 +547,33 @@ struct OpNonneg {
     }
 };
 
+// The last inner CGLS step of a TV outer iteration (solvers.py:450-459): only
+// u += alpha p survives it -- s = adj(r), gamma, beta and p are never read
+// again (u is returned, the next outer restarts from r = b - fwd(u)), so
+// that step is this one pass (+ the nonneg projection of solvers.py:414),
+// with the arithmetic of OpTvStepS's u update.
+template <typename V>
+struct OpTvAxpy {
+    V* u;
+    const V* p;
+    const Unit* us;
+    int nonneg;
+    struct In { V x, pp; };
+    __device__ bool enabled(int b) const { return us[b].status != ST_PAD; }
+    __device__ In load(int, size_t i, long long) const { return In{u[i], p[i]}; }
+    __device__ void apply(int b, size_t i, long long, const In& v, double (&)[1]) const {
+        using T = typename Sc<V>::T;
+        const Unit& un = us[b];
+        V x = v.x;
+        if (un.stepped) x = mk<V>(x.x + (T)un.alpha[0] * v.pp.x, x.y + (T)un.alpha[1] * v.pp.y);
+        if (nonneg) {
+            x.x = pos_(x.x);
+            x.y = pos_(x.y);
+        }
+        if (un.stepped || nonneg) u[i] = x;
+    }
+};
+
 template <typename R>
 struct OpAbsMax {  // per-channel max |deapo*y*scale| (TV default mu, solvers.py:364-372)
     using C = typename CT<R>::T;
@@ -1857,6 +1884,10 @@ struct Solver {
                 SPTB_TRY(grid<2>(OpTvGradNorm<C>{G, us, X, Y}, sums2));
                 k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
                 SPTB_TRY(unit_kernel_done());
+                if (j == inner - 1) {  // only u += alpha p is live (OpTvAxpy)
+                    SPTB_TRY(grid<0>(OpTvAxpy<C>{U, G, us, cfg.nonneg ? 1 : 0}, nullptr));
+                    break;
+                }
                 SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));     // rho_a -= alpha A p (in place)
                 SPTB_TRY(adjoint_grid(RH, true));
                 // u += alpha p ; rho -= alpha grad p ; s ; <s,s>  (W = s)
@@ -1867,7 +1898,6 @@ struct Solver {
                 SPTB_TRY(unit_kernel_done());
                 SPTB_TRY(grid<2>(OpTvS<R, 2, C>{W, G, ra, rb, deapo(), invP, us, X, Y}, nullptr));
             }
-            if (cfg.nonneg) SPTB_TRY(grid<0>(OpNonneg<C>{U, us}, nullptr));
             // shrink + Bregman + the next stacked target; W = deapo u; non-finite u
             SPTB_TRY(grid<1>(OpTvShrink<R, C>{U, rx, ry, bx, by, W, deapo(), us, X, Y}, sums3));
             // residual b - A u (reused as the next outer rho_a: same u)
