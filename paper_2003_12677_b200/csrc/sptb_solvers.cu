@@ -45,6 +45,7 @@ enum UnitStatus { RUNNING = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_NONFINITE =
 struct Unit {
     double alpha[2], alpha0[2], beta[2], gamma[2], gamma0[2], bnorm[2];
     double mu[2], lam[2];
+    double kap[2];  // TV shrink threshold 1 / lam
     double min_res;
     int act[2];      // per-channel activity of the current CG step
     int status;      // UnitStatus
@@ -452,6 +453,105 @@ k_sirt_adjpost_rowfft(const float2* __restrict__ w, float2* __restrict__ g, cons
     }
 }
 
+// A TV element pass fused with the x passes of the FFT2 around it (complex64,
+// X = 2^LOGN, 4 grid rows of one unit per CTA): INV_IN: W row -> IFFT_x ->
+// the op's y (the inverse y pass ran before); FWD_OUT: the op's W values ->
+// FFT_x -> W row (the forward y pass follows), else the values are stored.
+// Replaces IFFT_x + op + FFT_x (three passes over W) by one.  The row lives
+// in the CTA's shared row buffer between the transforms, so the element
+// loop holds no FFT registers: lane j takes x = j + TP k (coalesced), the
+// op's loads of Op::kUnroll elements in flight together, as in k_grid (a
+// first version kept the 16 transform values in registers: 128 registers,
+// one element's stencil loads in flight per thread, 3.5 ms per outer
+// iteration slower than the unfused passes).  The op's K sums are reduced
+// per CTA in a fixed order into part[(y0 / 4 * B + b) * K + k] for k_finish
+// (deterministic).
+template <int LOGN, bool INV_IN, bool FWD_OUT, int K, class Op>
+__global__ void __launch_bounds__(4 * (1 << LOGN) / 16, 1024 / (4 * (1 << LOGN) / 16))
+k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const float2* __restrict__ tw,
+            double* __restrict__ part) {
+    using namespace fftcore;
+    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, NT = 4 * TP;
+    constexpr int U = OpUnroll<Op>::value;
+    static_assert(16 % U == 0, "unroll divides 16");
+    extern __shared__ __align__(16) float2 tv_fbuf[];
+    __shared__ double red[K][NT / 32];
+    const int rb = threadIdx.x / TP, j = threadIdx.x % TP;
+    const long long gr0 = (long long)blockIdx.x * 4;
+    const int b = (int)(gr0 / Y), y0 = (int)(gr0 - (long long)b * Y), y = y0 + rb;
+    const size_t base = (size_t)b * M + (size_t)y * N;
+    float2* row = tv_fbuf + rb * N;
+    const bool en = op.enabled(b);  // CTA-uniform
+    if constexpr (INV_IN) {
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = w[base + j + TP * r];
+        dft16<true>(v);
+        fft16_stages<LOGN, true>(v, row, j, tw);
+        __syncthreads();  // stage 3 read other lanes' slots
+#pragma unroll
+        for (int q = 0; q < NB3; ++q)
+#pragma unroll
+            for (int r = 0; r < R3; ++r) row[j + TP * q + 256 * r] = v[q * R3 + r];
+        // lane j reads back only its own slots x = j + TP k: no barrier
+    }
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0;
+#pragma unroll 1
+    for (int k0 = 0; k0 < 16; k0 += U) {
+        typename Op::In in[U];
+        if (en) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int x = j + TP * (k0 + u);
+                if constexpr (INV_IN) {
+                    in[u] = op.load_nw(b, base + x, (long long)y * N + x);
+                    in[u].y = row[x];
+                } else {
+                    in[u] = op.load(b, base + x, (long long)y * N + x);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int x = j + TP * (k0 + u);
+            float2 val;
+            if (en) val = op.value(b, base + x, (long long)y * N + x, in[u], acc);
+            else if constexpr (INV_IN) val = row[x];
+            else val = w[base + x];
+            if constexpr (FWD_OUT) row[x] = val;
+            else w[base + x] = val;
+        }
+    }
+    if constexpr (FWD_OUT) {
+        float2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = row[j + TP * r];  // own slots
+        __syncthreads();  // fft16_stages overwrites other lanes' slots
+        dft16<false>(v);
+        fft16_stages<LOGN, false>(v, row, j, tw);
+#pragma unroll
+        for (int q = 0; q < NB3; ++q)
+#pragma unroll
+            for (int r = 0; r < R3; ++r) w[base + j + TP * q + 256 * r] = v[q * R3 + r];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double t = acc[k];
+#pragma unroll
+        for (int s = 16; s; s >>= 1) t += __shfl_down_sync(0xffffffffu, t, s);
+        if (lane == 0) red[k][warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double t = 0;
+        for (int u = 0; u < NT / 32; ++u) t += red[threadIdx.x][u];
+        part[((size_t)(y0 / 4) * B + b) * K + threadIdx.x] = t;
+    }
+}
+
 template <typename R, typename V>
 struct OpDeapo {  // w = deapo * v * scale  (v of any precision, w of plan precision)
     using C = typename CT<R>::T;
@@ -796,7 +896,7 @@ struct OpCgsDir {  // q = r + beta h ; p = q + beta (h + beta p) ; W = deapo p
 // 2: W holds s (MODE 1's): p = s + beta p, W = deapo p
 template <typename R, int MODE, typename V>
 struct OpTvS {
-    static constexpr int kUnroll = TV_UNROLL;
+    static constexpr int kUnroll = MODE == 2 ? 4 : TV_UNROLL;  // MODE 2: 3 loads per element
     using C = typename CT<R>::T;
     C* w;
     V* p;
@@ -807,15 +907,21 @@ struct OpTvS {
     int X, Y;
     struct In { C y; Bwd<V> g; V pp; R d; };
     __device__ bool enabled(int b) const { return MODE == 1 || us[b].active; }
-    __device__ In load(int, size_t i, long long m) const {
+    // every input but y (the fused x passes supply y from registers)
+    __device__ In load_nw(int, size_t i, long long m) const {
         In v;
-        v.y = w[i];
         if (MODE != 2) v.g = load_bwd(rx, ry, i, m, X, Y);
         if (MODE == 2) v.pp = p[i];
         v.d = deapo[m];
         return v;
     }
-    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
+    __device__ In load(int b, size_t i, long long m) const {
+        In v = load_nw(b, i, m);
+        v.y = w[i];
+        return v;
+    }
+    // the new W element (stored by apply(), or fed to a fused forward x pass)
+    __device__ C value(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         using T = typename Sc<V>::T;
         const Unit& un = us[b];
         const T d = (T)v.d;
@@ -826,8 +932,7 @@ struct OpTvS {
                 pp.y = (T)v.y.y + (T)un.beta[1] * pp.y;
                 p[i] = pp;
             }
-            w[i] = rc<R>(pp.x * d, pp.y * d);
-            return;
+            return rc<R>(pp.x * d, pp.y * d);
         }
         const T ds = (T)(v.d * scale);
         const V gt = v.g.gt();
@@ -837,10 +942,12 @@ struct OpTvS {
         acc[1] += (double)s.y * (double)s.y;
         if (MODE == 0) {
             p[i] = s;
-            w[i] = rc<R>(s.x * d, s.y * d);
-        } else {
-            w[i] = rc<R>(s.x, s.y);
+            return rc<R>(s.x * d, s.y * d);
         }
+        return rc<R>(s.x, s.y);
+    }
+    __device__ void apply(int b, size_t i, long long m, const In& v, double (&acc)[2]) const {
+        w[i] = value(b, i, m, v, acc);
     }
 };
 
@@ -878,7 +985,12 @@ struct OpTvStepS {
     int X, Y;
     struct In { C y; V pc, pr, pd, pl, pu, xc, xl, yc, yu, uu; R d; bool hr, hd, hl, hu; };
     __device__ bool enabled(int) const { return true; }
-    __device__ In load(int, size_t i, long long m) const {
+    __device__ In load(int b, size_t i, long long m) const {
+        In v = load_nw(b, i, m);
+        v.y = w[i];
+        return v;
+    }
+    __device__ In load_nw(int, size_t i, long long m) const {
         int x, y;
         split_m(m, X, x, y);
         In v;
@@ -886,7 +998,6 @@ struct OpTvStepS {
         v.hd = y < Y - 1;
         v.hl = x > 0;
         v.hu = y > 0;
-        v.y = w[i];
         v.pc = p[i];
         v.pr = p[v.hr ? i + 1 : i];
         v.pd = p[v.hd ? i + X : i];
@@ -900,7 +1011,10 @@ struct OpTvStepS {
         v.d = deapo[m];
         return v;
     }
-    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
+    __device__ void apply(int b, size_t i, long long m, const In& v, double (&acc)[2]) const {
+        w[i] = value(b, i, m, v, acc);
+    }
+    __device__ C value(int b, size_t i, long long, const In& v, double (&acc)[2]) const {
         using T = typename Sc<V>::T;
         const Unit& un = us[b];
         const bool st = un.stepped;
@@ -927,7 +1041,7 @@ struct OpTvStepS {
                           (T)un.mu[1] * ((T)v.y.y * ds) - (T)un.lam[1] * im);
         acc[0] += (double)s.x * (double)s.x;
         acc[1] += (double)s.y * (double)s.y;
-        w[i] = rc<R>(s.x, s.y);
+        return rc<R>(s.x, s.y);
     }
 };
 
@@ -950,20 +1064,23 @@ struct OpTvShrink {
     __device__ In load(int, size_t i, long long m) const {
         return In{load_fwd(u, i, m, X, Y), bx[i], by[i], deapo[m]};
     }
-    __device__ void apply(int b, size_t i, long long, const In& in, double (&acc)[1]) const {
+    __device__ void apply(int b, size_t i, long long m, const In& in, double (&acc)[1]) const {
+        w[i] = value(b, i, m, in, acc);
+    }
+    __device__ C value(int b, size_t i, long long, const In& in, double (&acc)[1]) const {
         using T = typename Sc<V>::T;
         const Unit& un = us[b];
         const V x = in.f.c, gx = in.f.gx(), gy = in.f.gy();
         if (!(isfinite(x.x) && isfinite(x.y))) acc[0] += 1.0;
         const T d = (T)in.d;
-        w[i] = rc<R>(x.x * d, x.y * d);
-        if (!un.active) return;
+        const C wv = rc<R>(x.x * d, x.y * d);
+        if (!un.active) return wv;
         const T vx[2] = {gx.x + in.bx.x, gx.y + in.bx.y};
         const T vy[2] = {gy.x + in.by.x, gy.y + in.by.y};
         T ox[2], oy[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const T kap = (T)(1.0 / un.lam[c]);
+            const T kap = (T)un.kap[c];  // 1 / lam (k_tv_mu)
             const T mag = sqrt(vx[c] * vx[c] + vy[c] * vy[c]);
             const T f = (mag - kap > (T)0 ? mag - kap : (T)0) / (mag > (T)0 ? mag : (T)1);
             ox[c] = vx[c] * f;
@@ -975,6 +1092,7 @@ struct OpTvShrink {
         by[i] = nby;
         rx[i] = mk<V>(ox[0] - nbx.x - gx.x, ox[1] - nbx.y - gx.y);
         ry[i] = mk<V>(oy[0] - nby.x - gy.x, oy[1] - nby.y - gy.y);
+        return wv;
     }
 };
 
@@ -1371,6 +1489,7 @@ __global__ void k_tv_mu(Unit* us, const double* mx, double cfg_mu, int B) {
         un.mu[1] = un.mu[0];
         un.lam[1] = un.lam[0];
     }
+    for (int c = 0; c < 2; ++c) un.kap[c] = 1.0 / un.lam[c];
 }
 
 __global__ void k_tv_inner_begin(Unit* us, const double* ss, int B) {
@@ -1528,7 +1647,9 @@ struct Solver {
         }
         nblk_grid = std::max(1, 1184 / B);
         nblk_spec = p->T * SPEC_Q;
-        const size_t np = (size_t)std::max(nblk_grid, nblk_spec) * B * 4;
+        // partial sums: k_grid (nblk_grid blocks), k_spec (nblk_spec) and the
+        // fused x passes (Y / 4 row groups), up to 4 sums per unit
+        const size_t np = (size_t)std::max({nblk_grid, nblk_spec, (int)(p->Y / 4)}) * B * 4;
         SPTB_TRY(alloc((void**)&part, sizeof(double) * np));
         SPTB_TRY(alloc((void**)&sums, sizeof(double) * B * 4));
         SPTB_TRY(alloc((void**)&sums2, sizeof(double) * B * 4));
@@ -1655,6 +1776,54 @@ struct Solver {
             (void)scale;
             return fail(SPTB_ERR_STATE, "sirt fused pass: complex64 only");
         }
+    }
+
+    // TV element passes fused with the FFT2 x passes (k_tv_rowfft)
+    bool tv_fused_ok() const {
+        return sizeof(R) == 4 && fft2_inplace_ok(p, W) && p->Y % 4 == 0 && !switches().tv_unfused;
+    }
+    template <bool INV_IN, bool FWD_OUT, int K, class Op>
+    int tv_row(const Op& op, double* out_sums) {
+        if constexpr (sizeof(R) == 4) {
+            const int L = fft2_log2(p->X);
+            const float2* tw = fft2_twiddles(p, L);
+            if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
+            const unsigned grid = (unsigned)((long long)B * p->Y / 4);
+            auto run = [&](auto kern, int logn) -> int {
+                const int nt = 4 * (1 << logn) / 16, sm = (int)(sizeof(float2) * 4 * (1 << logn));
+                SPTB_CUDA(set_smem_once((const void*)kern, sm, -1));
+                kern<<<grid, nt, sm, st>>>(op, (float2*)W, p->M, p->Y, B, tw, part);
+                SPTB_LAUNCHED();
+                return SPTB_OK;
+            };
+            switch (L) {
+                case 9: SPTB_TRY(run(k_tv_rowfft<9, INV_IN, FWD_OUT, K, Op>, 9)); break;
+                case 10: SPTB_TRY(run(k_tv_rowfft<10, INV_IN, FWD_OUT, K, Op>, 10)); break;
+                case 11: SPTB_TRY(run(k_tv_rowfft<11, INV_IN, FWD_OUT, K, Op>, 11)); break;
+                case 12: SPTB_TRY(run(k_tv_rowfft<12, INV_IN, FWD_OUT, K, Op>, 12)); break;
+                default: return fail(SPTB_ERR_ARG, "tv fused pass: unsupported n_x");
+            }
+            if (out_sums) {
+                k_finish<<<(B * K * 32 + 255) / 256, 256, 0, st>>>(part, p->Y / 4, B, K, 0, out_sums);
+                SPTB_LAUNCHED();
+            }
+            return SPTB_OK;
+        } else {
+            (void)op;
+            (void)out_sums;
+            return fail(SPTB_ERR_STATE, "tv fused pass: complex64 only");
+        }
+    }
+    // S_(w) rh -> W and the inverse y pass (the x pass is fused into the next op)
+    int adjoint_cols(const C* rh) {
+        const void* vals = p->SW_val ? p->SW_val : p->S.val;
+        SPTB_TRY(launch_spmm_s<R>(p, vals, rh, W, B, st));
+        return launch_fft2_cols(p, W, B, true, st);
+    }
+    // the forward y pass of W (x pass done) and S^H: out = (sub -) S^H W
+    int forward_cols(C* out, const C* sub) {
+        SPTB_TRY(launch_fft2_cols(p, W, B, false, st));
+        return launch_spmm_sh_patch<R>(p, W, out, B, sub, st);
     }
 
     // out[s][b] = (sub ? sub - : ) S^H FFT2(W)    (W holds deapo*v, [b][m]; clobbered)
@@ -1846,6 +2015,47 @@ struct Solver {
     }
 
     // ---------------------------------------------------------------- TV
+    // One outer iteration with the element passes fused into the FFT2 x
+    // passes (same algorithm and arithmetic as the unfused body in run_tv;
+    // the sums are reduced per grid row group instead of per k_grid block)
+    int tv_outer_fused(int inner, double invP, int it, int nonneg, double tol) {
+        const int X = p->X, Y = p->Y;
+        // r = target - fwd(u), s = adj(r), p = s: IFFT_x + OpTvS<0> + FFT_x
+        SPTB_TRY(adjoint_cols(RH));
+        SPTB_TRY((tv_row<true, true, 2>(OpTvS<R, 0, C>{W, G, rx, ry, deapo(), invP, us, X, Y}, sums2)));
+        k_tv_inner_begin<<<1, 64, 0, st>>>(us, sums2, B);
+        SPTB_TRY(unit_kernel_done());
+        C *ra = rx, *rb = ry, *wa = rx2, *wb = ry2;
+        for (int j = 0; j < inner; ++j) {
+            SPTB_TRY(forward_cols(QH, nullptr));  // Qhat = F(p) (x pass done)
+            SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
+            SPTB_TRY(grid<2>(OpTvGradNorm<C>{G, us, X, Y}, sums2));
+            k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
+            SPTB_TRY(unit_kernel_done());
+            if (j == inner - 1) {
+                SPTB_TRY(grid<0>(OpTvAxpy<C>{U, G, us, nonneg}, nullptr));
+                break;
+            }
+            SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));
+            SPTB_TRY(adjoint_cols(RH));
+            // IFFT_x + the step (u, rho) + s -> W
+            SPTB_TRY((tv_row<true, false, 2>(OpTvStepS<R, C>{W, U, G, ra, rb, wa, wb, deapo(), invP, us, X, Y},
+                                             sums2)));
+            std::swap(ra, wa);
+            std::swap(rb, wb);
+            k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 1);
+            SPTB_TRY(unit_kernel_done());
+            // p = s + beta p ; FFT_x(deapo p)
+            SPTB_TRY((tv_row<false, true, 2>(OpTvS<R, 2, C>{W, G, ra, rb, deapo(), invP, us, X, Y}, nullptr)));
+        }
+        // shrink + Bregman + next target; FFT_x(deapo u); residual b - A u
+        SPTB_TRY((tv_row<false, true, 1>(OpTvShrink<R, C>{U, rx, ry, bx, by, W, deapo(), us, X, Y}, sums3)));
+        SPTB_TRY(forward_cols(RH, BH));
+        SPTB_TRY(spec<false>(RH, (const C*)nullptr, (C*)nullptr, sums));
+        k_tv_check<<<1, 64, 0, st>>>(us, sums, sums3, p->P, it, B, hist, tol);
+        return unit_kernel_done();
+    }
+
     int run_tv(const sptb_solver_config& cfg) {
         const double invP = 1.0 / p->P;
         const int X = p->X, Y = p->Y;
@@ -1864,10 +2074,15 @@ struct Solver {
         // stacked CGLS restarts every outer iteration after 2 steps
         SPTB_CUDA(cudaMemcpyAsync(RH, BH, sizeof(C) * (size_t)B * p->N, cudaMemcpyDeviceToDevice, st));
         const int inner = std::max(1, cfg.tv_inner_iter);
+        const bool fused = tv_fused_ok();
         for (int it = 0; it < cfg.max_iter; ++it) {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            if (fused) {
+                SPTB_TRY(iterate(it, [&]() -> int { return tv_outer_fused(inner, invP, it, cfg.nonneg, cfg.tol); }));
+                continue;
+            }
             SPTB_TRY(iterate(it, [&]() -> int {
             // stacked CGLS on (sqrt(mu) A; sqrt(lam) grad) u = (sqrt(mu) b; sqrt(lam)(d - b));
             // rho = (d - b) - grad u comes from the previous shrink pass (0 at u = 0)

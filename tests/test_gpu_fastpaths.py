@@ -214,3 +214,46 @@ def test_sirt_fused_passes_other_grids(sb, n, T, nx, ny):
     assert [r.iterations_run for r in rep] == [r.iterations_run for r in rep2]
     assert rel(np.asarray(rec.cpu() if hasattr(rec, "cpu") else rec),
                np.asarray(rec2.cpu() if hasattr(rec2, "cpu") else rec2)) < 1e-4
+
+
+@pytest.mark.parametrize("n,T,nx,ny,inner,nonneg", [
+    (512, 96, None, None, 2, False), (512, 96, None, None, 3, True), (512, 96, None, None, 1, False),
+    (4096, 6, None, None, 2, False), (1024, 24, 512, 2048, 2, True), (512, 45, 1024, 512, 2, False)])
+def test_tv_fused_passes_match_unfused(sb, n, T, nx, ny, inner, nonneg):
+    """The TV element passes fused into the FFT2 x passes (k_tv_rowfft: IFFT_x
+    + OpTvS + FFT_x, IFFT_x + OpTvStepS, OpTvS + FFT_x, OpTvShrink + FFT_x) vs
+    the separate element passes and FFT2 (SPTB_TV_UNFUSED), both against the
+    complex128 build: same iterations, and the fused result as close to the
+    complex128 one as the unfused (max(1e-4, 3x its deviation): complex64 TV
+    moves by ~1e-3 under rounding-level changes where the shrink threshold
+    cuts many pixels) -- including 1 and 3 inner steps, the nonneg
+    projection, 4096-wide rows and rectangular grids."""
+    import torch
+    from oracle import shepp_logan
+    from paper_2003_12677_b200.solvers import solve_batch
+    geom = sb.ScanGeometry(n_p=n, n_theta=T, n_x=nx, n_y=ny)
+    ops = sb.build_operators(geom, filter_kind="none", max_batch=4)
+    if nx is None:
+        img = torch.from_numpy(shepp_logan(n, 8).astype(np.float32)).cuda()
+        img = img * torch.linspace(0.5, 1.5, 8, device="cuda")[:, None, None]
+    else:
+        g = torch.Generator(device="cuda").manual_seed(n + T + inner)
+        img = torch.rand(8, ops.geom.n_y, ops.geom.n_x, device="cuda", generator=g)
+    sino = ops.radon(img)
+    cfg = sb.SolverConfig(algorithm="tv", max_iter=4, tv_inner_iter=inner, nonneg=nonneg)
+
+    def host(r):
+        return np.asarray(r.cpu() if hasattr(r, "cpu") else r, dtype=np.float64)
+
+    rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    with _env("SPTB_TV_UNFUSED", "1"):
+        rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    ops64 = sb.build_operators(geom, filter_kind="none", max_batch=4, precision="complex128")
+    rec3, rep3, _ = solve_batch(sino.double().cpu().numpy(), ops64, cfg, raise_on_failure=False)
+    its = [[r.iterations_run for r in x] for x in (rep, rep2, rep3)]
+    assert its[0] == its[1] == its[2] == [4] * len(rep), (its, [r.__dict__ for r in rep])
+    a, b, c = host(rec), host(rec2), host(rec3)
+    assert np.isfinite(a).all()
+    ea, eb = rel(a, c), rel(b, c)
+    print(f"fused {ea:.2e} unfused {eb:.2e} from complex128")
+    assert ea <= max(1e-4, 3 * eb), (ea, eb)
