@@ -140,7 +140,7 @@ struct Switches {
     bool fft2_no_persist = false, fft2_no_bulk = false;
     bool fft1_stockham = false, fft1_no_bulk = false, fft1_r16_inv = false;
     bool fft1_inv_gather = false, fft1_fwd_rows = false, fft1_perm = false;
-    bool sirt_unfused = false, tv_unfused = false, spmm_rows = false, no_graph = false;
+    bool sirt_unfused = false, xpass_unfused = false, spmm_rows = false, no_graph = false;
     int sh_grid = 0;       // S^H launch grid override (0: default)
     int pipe_chunks = 0;   // host pipeline chunks per call (0: default)
 };

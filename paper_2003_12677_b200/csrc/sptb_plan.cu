@@ -40,7 +40,7 @@ void reload_switches() {
     s.fft1_fwd_rows = env_on("SPTB_FFT1_FWD_ROWS");
     s.fft1_perm = env_on("SPTB_FFT1_PERM");
     s.sirt_unfused = env_on("SPTB_SIRT_UNFUSED");
-    s.tv_unfused = env_on("SPTB_TV_UNFUSED");
+    s.xpass_unfused = env_on("SPTB_XPASS_UNFUSED");
     s.spmm_rows = env_on("SPTB_SPMM_ROWS");
     s.no_graph = env_on("SPTB_NO_GRAPH");
     s.pipe_chunks = std::max(0, env_int("SPTB_PIPE_CHUNKS"));

@@ -701,14 +701,22 @@ struct OpCglsInit {  // p = s = deapo*y*scale ; <s,s> ; W = deapo p
     double scale;
     struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
+    __device__ In load_nw(int, size_t, long long m) const {
+        In v;
+        v.d = deapo[m];
+        return v;
+    }
     __device__ In load(int, size_t i, long long m) const { return In{w[i], deapo[m]}; }
-    __device__ void apply(int, size_t i, long long, const In& v, double (&acc)[2]) const {
+    __device__ C value(int, size_t i, long long, const In& v, double (&acc)[2]) const {
         const double d = (double)v.d;
         const D2 s = make_double2(v.y.x * d * scale, v.y.y * d * scale);
         acc[0] += s.x * s.x;
         acc[1] += s.y * s.y;
         p[i] = tv_store<V>(s.x, s.y);
-        w[i] = rc<R>(s.x * d, s.y * d);
+        return rc<R>(s.x * d, s.y * d);
+    }
+    __device__ void apply(int b, size_t i, long long m, const In& v, double (&acc)[2]) const {
+        w[i] = value(b, i, m, v, acc);
     }
 };
 
@@ -720,12 +728,22 @@ struct OpDotS {  // <s,s>, s = deapo*y*scale
     double scale;
     struct In { C y; R d; };
     __device__ bool enabled(int) const { return true; }
+    __device__ In load_nw(int, size_t, long long m) const {
+        In v;
+        v.d = deapo[m];
+        return v;
+    }
     __device__ In load(int, size_t i, long long m) const { return In{y[i], deapo[m]}; }
-    __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
+    // fused after the inverse x pass: the row y is stored unchanged
+    __device__ C value(int, size_t, long long, const In& v, double (&acc)[2]) const {
         const double d = (double)v.d * scale;
         const double sx = v.y.x * d, sy = v.y.y * d;
         acc[0] += sx * sx;
         acc[1] += sy * sy;
+        return v.y;
+    }
+    __device__ void apply(int b, size_t i, long long m, const In& v, double (&acc)[2]) const {
+        (void)value(b, i, m, v, acc);
     }
 };
 
@@ -741,7 +759,10 @@ struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-fi
     struct In { V x, pp; C y; R d; };
     __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const { return In{u[i], p[i], w[i], deapo[m]}; }
-    __device__ void apply(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
+    __device__ void apply(int b, size_t i, long long m, const In& v, double (&acc)[1]) const {
+        w[i] = value(b, i, m, v, acc);
+    }
+    __device__ C value(int b, size_t i, long long, const In& v, double (&acc)[1]) const {
         const Unit& un = us[b];
         D2 x = d2(v.x);
         D2 pp = d2(v.pp);
@@ -757,7 +778,7 @@ struct OpCglsTail {  // u += alpha p ; p = s + beta p ; W = deapo p_new ; non-fi
             }
         }
         if (!finite2(x.x, x.y)) acc[0] += 1.0;
-        w[i] = rc<R>(pp.x * d, pp.y * d);
+        return rc<R>(pp.x * d, pp.y * d);
     }
 };
 
@@ -1780,7 +1801,7 @@ struct Solver {
 
     // TV element passes fused with the FFT2 x passes (k_tv_rowfft)
     bool tv_fused_ok() const {
-        return sizeof(R) == 4 && fft2_inplace_ok(p, W) && p->Y % 4 == 0 && !switches().tv_unfused;
+        return sizeof(R) == 4 && fft2_inplace_ok(p, W) && p->Y % 4 == 0 && !switches().xpass_unfused;
     }
     template <bool INV_IN, bool FWD_OUT, int K, class Op>
     int tv_row(const Op& op, double* out_sums) {
@@ -1938,14 +1959,43 @@ struct Solver {
         // u, p and the spectral residual are stored in the plan's type (the
         // passes are HBM-bound), the recurrence arithmetic is fp64
         SPTB_CUDA(cudaMemcpyAsync(RH, BH, sizeof(C) * (size_t)B * p->N, cudaMemcpyDeviceToDevice, st));
-        SPTB_TRY(adjoint_grid(BH, true));
-        SPTB_TRY(grid<2>(OpCglsInit<R, C>{W, G, deapo(), invP}, sums2));
+        // fused: the element passes share the FFT2 x passes (k_tv_rowfft), W
+        // leaves every iteration x-transformed for the next forward y pass
+        const bool fused = tv_fused_ok();
+        if (fused) {
+            SPTB_TRY(adjoint_cols(BH));
+            SPTB_TRY((tv_row<true, true, 2>(OpCglsInit<R, C>{W, G, deapo(), invP}, sums2)));
+        } else {
+            SPTB_TRY(adjoint_grid(BH, true));
+            SPTB_TRY(grid<2>(OpCglsInit<R, C>{W, G, deapo(), invP}, sums2));
+        }
         k_cgls_init<<<1, 64, 0, st>>>(us, sums2, B);
         SPTB_TRY(unit_kernel_done());
         for (int it = 0; it < cfg.max_iter; ++it) {
             bool stop;
             SPTB_TRY(poll(it, &stop));
             if (stop) break;
+            if (fused) {
+                SPTB_TRY(iterate(it, [&]() -> int {
+                SPTB_TRY(forward_cols(QH, nullptr));
+                SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
+                k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, nullptr, p->P, B, 0);
+                SPTB_TRY(unit_kernel_done());
+                SPTB_TRY(spec<true>(RH, QH, (C*)nullptr, sums));
+                k_cgls_check<<<1, 64, 0, st>>>(us, sums, p->P, it, B, hist, cfg.tol);
+                SPTB_TRY(unit_kernel_done());
+                // s = A^H W r: IFFT_x + gamma_new
+                SPTB_TRY(adjoint_cols(RH));
+                SPTB_TRY((tv_row<true, false, 2>(OpDotS<R>{W, deapo(), invP}, sums2)));
+                k_cgls_beta<<<1, 64, 0, st>>>(us, sums2, B, 0);
+                SPTB_TRY(unit_kernel_done());
+                // u += alpha p ; p = s + beta p ; FFT_x(deapo p_new)
+                SPTB_TRY((tv_row<false, true, 1>(OpCglsTail<R, C>{U, G, W, deapo(), invP, us}, sums3)));
+                k_flag_nonfinite<<<1, 64, 0, st>>>(us, sums3, B, 1);
+                return unit_kernel_done();
+                }));
+                continue;
+            }
             SPTB_TRY(iterate(it, [&]() -> int {
             // q = A p  -> delta, alpha, activity
             SPTB_TRY(forward_spec(QH, nullptr));

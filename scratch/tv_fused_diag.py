@@ -10,8 +10,8 @@ def rel(a, b):
     return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
 
 def run(ops, sino, cfg, unfused):
-    if unfused: os.environ["SPTB_TV_UNFUSED"] = "1"
-    else: os.environ.pop("SPTB_TV_UNFUSED", None)
+    if unfused: os.environ["SPTB_XPASS_UNFUSED"] = "1"
+    else: os.environ.pop("SPTB_XPASS_UNFUSED", None)
     _lib.lib.sptb_reload_switches()
     rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
     rec = rec.cpu().numpy() if hasattr(rec, "cpu") else np.asarray(rec)

@@ -222,7 +222,7 @@ def test_sirt_fused_passes_other_grids(sb, n, T, nx, ny):
 def test_tv_fused_passes_match_unfused(sb, n, T, nx, ny, inner, nonneg):
     """The TV element passes fused into the FFT2 x passes (k_tv_rowfft: IFFT_x
     + OpTvS + FFT_x, IFFT_x + OpTvStepS, OpTvS + FFT_x, OpTvShrink + FFT_x) vs
-    the separate element passes and FFT2 (SPTB_TV_UNFUSED), both against the
+    the separate element passes and FFT2 (SPTB_XPASS_UNFUSED), both against the
     complex128 build: same iterations, and the fused result as close to the
     complex128 one as the unfused (max(1e-4, 3x its deviation): complex64 TV
     moves by ~1e-3 under rounding-level changes where the shrink threshold
@@ -246,7 +246,7 @@ def test_tv_fused_passes_match_unfused(sb, n, T, nx, ny, inner, nonneg):
         return np.asarray(r.cpu() if hasattr(r, "cpu") else r, dtype=np.float64)
 
     rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
-    with _env("SPTB_TV_UNFUSED", "1"):
+    with _env("SPTB_XPASS_UNFUSED", "1"):
         rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
     ops64 = sb.build_operators(geom, filter_kind="none", max_batch=4, precision="complex128")
     rec3, rep3, _ = solve_batch(sino.double().cpu().numpy(), ops64, cfg, raise_on_failure=False)
@@ -257,3 +257,44 @@ def test_tv_fused_passes_match_unfused(sb, n, T, nx, ny, inner, nonneg):
     ea, eb = rel(a, c), rel(b, c)
     print(f"fused {ea:.2e} unfused {eb:.2e} from complex128")
     assert ea <= max(1e-4, 3 * eb), (ea, eb)
+
+
+@pytest.mark.parametrize("n,T,nx,ny,nonneg", [
+    (512, 96, None, None, False), (512, 96, None, None, True), (4096, 6, None, None, False),
+    (1024, 24, 512, 2048, False), (512, 45, 1024, 512, True)])
+def test_cgls_fused_passes_match_unfused(sb, n, T, nx, ny, nonneg):
+    """CGLS with its element passes fused into the FFT2 x passes (IFFT_x +
+    OpCglsInit + FFT_x, IFFT_x + <s,s>, OpCglsTail + FFT_x) vs the separate
+    passes (SPTB_XPASS_UNFUSED), both against the complex128 build."""
+    import torch
+    from oracle import shepp_logan
+    from paper_2003_12677_b200.solvers import solve_batch
+    geom = sb.ScanGeometry(n_p=n, n_theta=T, n_x=nx, n_y=ny)
+    ops = sb.build_operators(geom, filter_kind="none", max_batch=4)
+    if nx is None:
+        img = torch.from_numpy(shepp_logan(n, 8).astype(np.float32)).cuda()
+    else:
+        g = torch.Generator(device="cuda").manual_seed(n + T)
+        img = torch.rand(8, ops.geom.n_y, ops.geom.n_x, device="cuda", generator=g)
+    sino = ops.radon(img)
+    cfg = sb.SolverConfig(algorithm="cgls", max_iter=8, nonneg=nonneg)
+
+    def host(r):
+        return np.asarray(r.cpu() if hasattr(r, "cpu") else r, dtype=np.float64)
+
+    rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    with _env("SPTB_XPASS_UNFUSED", "1"):
+        rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    ops64 = sb.build_operators(geom, filter_kind="none", max_batch=4, precision="complex128")
+    rec3, rep3, _ = solve_batch(sino.double().cpu().numpy(), ops64, cfg, raise_on_failure=False)
+    its = [[r.iterations_run for r in x] for x in (rep, rep2, rep3)]
+    assert its[0] == its[1] == its[2], its
+    a, b, c = host(rec), host(rec2), host(rec3)
+    assert np.isfinite(a).all()
+    ea, eb = rel(a, c), rel(b, c)
+    print(f"fused {ea:.2e} unfused {eb:.2e} from complex128")
+    assert ea <= max(1e-4, 3 * eb), (ea, eb)
+    # complex64 CGLS drifts from complex128 after a few steps (loss of
+    # orthogonality; fused and unfused alike): the early residuals agree
+    for r, r3 in zip(rep, rep3):
+        np.testing.assert_allclose(r.residual_history[:4], r3.residual_history[:4], rtol=1e-4)
