@@ -87,15 +87,20 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[K], double* out
     }
 }
 
-// partial[(blk*B + b)*K + k] -> sums[b*K + k]: one warp per output, lanes take
-// blk = lane, lane+32, ... and a fixed shuffle tree combines them (deterministic)
-__global__ void k_finish(const double* __restrict__ part, int nblk, int B, int K, int is_max,
-                         double* __restrict__ sums) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (w >= B * K) return;
+// partial[(blk*B + b)*K + k] -> sums[b*K + k]: one FT-thread block per
+// output, threads take blk = t, t + FT, ... and a fixed shuffle + shared
+// tree combines them (deterministic).  (One warp per output, 8 blocks for
+// 64 sums, left a k_spec finish -- 6144 partials per output -- as 192
+// dependent L2 round trips per lane on 8 SMs.)
+constexpr int FT = 128;
+__global__ void __launch_bounds__(FT) k_finish(const double* __restrict__ part, int nblk, int B, int K, int is_max,
+                                              double* __restrict__ sums) {
+    __shared__ double sh[FT / 32];
+    const int w = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = w / K, k = w % K;
     double s = 0;
-    for (int blk = lane; blk < nblk; blk += 32) {
+#pragma unroll 4
+    for (int blk = threadIdx.x; blk < nblk; blk += FT) {
         const double v = part[((size_t)blk * B + b) * K + k];
         s = is_max ? fmax(s, v) : s + v;
     }
@@ -103,7 +108,13 @@ __global__ void k_finish(const double* __restrict__ part, int nblk, int B, int K
         const double t = __shfl_down_sync(0xffffffffu, s, o);
         s = is_max ? fmax(s, t) : s + t;
     }
-    if (lane == 0) sums[w] = s;
+    if (lane == 0) sh[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = sh[0];
+        for (int u = 1; u < FT / 32; ++u) t = is_max ? fmax(t, sh[u]) : t + sh[u];
+        sums[w] = t;
+    }
 }
 
 // grid kernels: gridDim = (nblk, B); block-uniform unit b; element (b, m)
@@ -1703,7 +1714,7 @@ struct Solver {
         k_grid<K, MAX, Op><<<g, RT, 0, st>>>(op, p->M, part);
         SPTB_LAUNCHED();
         if (K > 0 && out_sums) {
-            k_finish<<<(B * K * 32 + 255) / 256, 256, 0, st>>>(part, nblk_grid, B, K, MAX ? 1 : 0,
+            k_finish<<<B * K, FT, 0, st>>>(part, nblk_grid, B, K, MAX ? 1 : 0,
                                                           out_sums);
             SPTB_LAUNCHED();
         }
@@ -1715,7 +1726,7 @@ struct Solver {
         k_spec<R, RV, UPDATE><<<nblk_spec, RT, 0, st>>>(rh, qh, rf, p->shp.perm, (const R*)p->w_dev, p->w_len,
                                                         p->T, p->P, B, us, part);
         SPTB_LAUNCHED();
-        k_finish<<<(B * 2 * 32 + 255) / 256, 256, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
+        k_finish<<<B * 2, FT, 0, st>>>(part, nblk_spec, B, 2, 0, out_sums);
         SPTB_LAUNCHED();
         return SPTB_OK;
     }
@@ -1790,7 +1801,7 @@ struct Solver {
                 case 12: SPTB_TRY(run(k_sirt_adjpost_rowfft<12>, 12)); break;
                 default: return fail(SPTB_ERR_ARG, "sirt fused pass: unsupported n_x");
             }
-            k_finish<<<(B * 4 * 32 + 255) / 256, 256, 0, st>>>(part, p->Y / 4, B, 4, 0, sums3);
+            k_finish<<<B * 4, FT, 0, st>>>(part, p->Y / 4, B, 4, 0, sums3);
             SPTB_LAUNCHED();
             return SPTB_OK;
         } else {
@@ -1825,7 +1836,7 @@ struct Solver {
                 default: return fail(SPTB_ERR_ARG, "tv fused pass: unsupported n_x");
             }
             if (out_sums) {
-                k_finish<<<(B * K * 32 + 255) / 256, 256, 0, st>>>(part, p->Y / 4, B, K, 0, out_sums);
+                k_finish<<<B * K, FT, 0, st>>>(part, p->Y / 4, B, K, 0, out_sums);
                 SPTB_LAUNCHED();
             }
             return SPTB_OK;
