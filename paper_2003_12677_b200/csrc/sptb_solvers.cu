@@ -136,6 +136,16 @@ struct OpUnroll<Op, std::void_t<decltype(Op::kUnroll)>> {
 #ifndef TV_UNROLL
 #define TV_UNROLL 2
 #endif
+// ops whose value() result is not a W element (reductions only): k_tv_rowfft
+// stores nothing for them
+template <class Op, class = void>
+struct OpStoresW {
+    static constexpr bool value = true;
+};
+template <class Op>
+struct OpStoresW<Op, std::void_t<decltype(Op::kNoW)>> {
+    static constexpr bool value = !Op::kNoW;
+};
 template <int K, bool MAX, class Op>
 __global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
     const int b = blockIdx.y;
@@ -532,7 +542,7 @@ k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const floa
             else if constexpr (INV_IN) val = row[x];
             else val = w[base + x];
             if constexpr (FWD_OUT) row[x] = val;
-            else w[base + x] = val;
+            else if constexpr (OpStoresW<Op>::value) w[base + x] = val;
         }
     }
     if constexpr (FWD_OUT) {
@@ -985,6 +995,7 @@ struct OpTvS {
 
 template <typename V>
 struct OpTvGradNorm {  // ||grad p||^2 per channel
+    static constexpr bool kNoW = true;
     const V* p;
     const Unit* us;
     int X, Y;
@@ -995,6 +1006,10 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
         const V gx = v.f.gx(), gy = v.f.gy();
         acc[0] += (double)(gx.x * gx.x + gy.x * gy.x);
         acc[1] += (double)(gx.y * gx.y + gy.y * gy.y);
+    }
+    __device__ float2 value(int b, size_t i, long long m, const In& v, double (&acc)[2]) const {
+        apply(b, i, m, v, acc);
+        return make_float2(0.f, 0.f);
     }
 };
 
@@ -1852,8 +1867,9 @@ struct Solver {
             if (!tw) return fail(SPTB_ERR_CUDA, "fft2: twiddle table");
             const unsigned grid = (unsigned)((long long)B * p->Y / 4);
             auto run = [&](auto kern, int logn) -> int {
-                const int nt = 4 * (1 << logn) / 16, sm = (int)(sizeof(float2) * 4 * (1 << logn));
-                SPTB_CUDA(set_smem_once((const void*)kern, sm, -1));
+                const int nt = 4 * (1 << logn) / 16;
+                const int sm = (INV_IN || FWD_OUT) ? (int)(sizeof(float2) * 4 * (1 << logn)) : 0;
+                if (sm) SPTB_CUDA(set_smem_once((const void*)kern, sm, -1));
                 kern<<<grid, nt, sm, st>>>(op, (float2*)W, p->M, p->Y, B, tw, part);
                 SPTB_LAUNCHED();
                 return SPTB_OK;
@@ -2120,7 +2136,8 @@ struct Solver {
         for (int j = 0; j < inner; ++j) {
             SPTB_TRY(forward_cols(QH, nullptr));  // Qhat = F(p) (x pass done)
             SPTB_TRY(spec<false>(QH, (const C*)nullptr, (C*)nullptr, sums));
-            SPTB_TRY(grid<2>(OpTvGradNorm<C>{G, us, X, Y}, sums2));
+            // ||grad p||^2 in 4-row groups (x, y known per lane)
+            SPTB_TRY((tv_row<false, false, 2>(OpTvGradNorm<C>{G, us, X, Y}, sums2)));
             k_cgls_alpha<<<1, 64, 0, st>>>(us, sums, sums2, p->P, B, 1);
             SPTB_TRY(unit_kernel_done());
             if (j == inner - 1) {
