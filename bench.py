@@ -245,9 +245,17 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: SPTB_BENCH_ONE_GPU=1 puts every rank on cuda:0 over gloo, so
+    # the multi-rank code path runs on a one-GPU box (not a measurement)
+    one_gpu = os.environ.get("SPTB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2003_12677_b200 as sb
     from paper_2003_12677_b200 import _lib
     from oracle import shepp_logan  # synthetic phantom generator only (io.py:130-148)
