@@ -2,9 +2,10 @@
 each data path -- every rank loads its own slices ("local"), rank 0
 scatters over NCCL ("scatter"), each rank writes its own slices into a shared
 memory-mapped volume ("out") -- gives the single-GPU result bit for bit (same
-launch batch on every rank, fixed-order reductions).  Skipped on boxes with
-fewer than 2 GPUs (the gloo tests in test_pipeline_dist.py cover the logic
-on CPU)."""
+launch batch on every rank, fixed-order reductions).  The NCCL cases are
+skipped on boxes with fewer than 2 GPUs; the gloo cases run two ranks on
+cuda:0 with the device solver (test_pipeline_dist.py covers the logic on
+CPU)."""
 
 import os
 import socket
@@ -36,13 +37,17 @@ def _stack():
     return sb.SinogramStack(data=data.astype(np.float32), geometry=geom)
 
 
-def _worker(rank, world, port, mode, out_path, q):
+def _worker(rank, world, port, mode, out_path, q, backend="nccl"):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    if backend == "gloo":  # both ranks on cuda:0: the host-side data paths
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
         import paper_2003_12677_b200 as sb
         stack = _stack() if (mode != "scatter" or rank == 0) else None
@@ -55,9 +60,7 @@ def _worker(rank, world, port, mode, out_path, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("mode", ["local", "scatter", "out"])
-def test_two_gpu_pipeline_bitwise(tmp_path, mode):
+def _run_two(tmp_path, mode, backend):
     import torch.multiprocessing as mp
     import paper_2003_12677_b200 as sb
     ops = sb.build_operators(sb.ScanGeometry(n_p=N, n_theta=T), filter_kind="hamming")
@@ -69,7 +72,7 @@ def test_two_gpu_pipeline_bitwise(tmp_path, mode):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, out_path, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, out_path, q, backend)) for r in range(2)]
     for p in procs:
         p.start()
     res = {r[0]: r for r in (q.get(timeout=300) for _ in procs)}
@@ -80,3 +83,16 @@ def test_two_gpu_pipeline_bitwise(tmp_path, mode):
     np.testing.assert_array_equal(vol, ref.data.astype(np.float32))
     np.testing.assert_array_equal(res[0][2], ref_rep.residual_history)
     assert res[0][3] == ref_rep.iterations_run and res[1][1] is None
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("mode", ["local", "scatter", "out"])
+def test_two_gpu_pipeline_bitwise(tmp_path, mode):
+    _run_two(tmp_path, mode, "nccl")
+
+
+@pytest.mark.parametrize("mode", ["local", "scatter", "out"])
+def test_two_ranks_one_gpu_pipeline_bitwise(tmp_path, mode):
+    """The same with both ranks on cuda:0 over gloo: the device solver under
+    run_pipeline's multi-rank host paths on a one-GPU box."""
+    _run_two(tmp_path, mode, "gloo")
