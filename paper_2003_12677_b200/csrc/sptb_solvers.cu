@@ -146,6 +146,23 @@ template <class Op>
 struct OpStoresW<Op, std::void_t<decltype(Op::kNoW)>> {
     static constexpr bool value = !Op::kNoW;
 };
+// ops that take the grid coordinates directly (no index split per element)
+template <class Op, class = void>
+struct OpLoadXY {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct OpLoadXY<Op, std::void_t<decltype(&Op::load_xy)>> {
+    static constexpr bool value = true;
+};
+template <class Op, class = void>
+struct OpLoadNwXY {
+    static constexpr bool value = false;
+};
+template <class Op>
+struct OpLoadNwXY<Op, std::void_t<decltype(&Op::load_nw_xy)>> {
+    static constexpr bool value = true;
+};
 template <int K, bool MAX, class Op>
 __global__ void __launch_bounds__(RT) k_grid(Op op, long long M, double* part) {
     const int b = blockIdx.y;
@@ -286,9 +303,7 @@ struct Fwd {  // centre, right (x+1), down (y+1); forward differences
     __device__ __forceinline__ V gy() const { return hd ? mk<V>(d.x - c.x, d.y - c.y) : mk<V>(0, 0); }
 };
 template <typename V>
-__device__ __forceinline__ Fwd<V> load_fwd(const V* v, size_t i, long long m, int X, int Y) {
-    int x, y;
-    split_m(m, X, x, y);
+__device__ __forceinline__ Fwd<V> load_fwd_xy(const V* v, size_t i, int x, int y, int X, int Y) {
     Fwd<V> f;
     f.hr = x < X - 1;
     f.hd = y < Y - 1;
@@ -296,6 +311,12 @@ __device__ __forceinline__ Fwd<V> load_fwd(const V* v, size_t i, long long m, in
     f.r = v[f.hr ? i + 1 : i];
     f.d = v[f.hd ? i + X : i];
     return f;
+}
+template <typename V>
+__device__ __forceinline__ Fwd<V> load_fwd(const V* v, size_t i, long long m, int X, int Y) {
+    int x, y;
+    split_m(m, X, x, y);
+    return load_fwd_xy(v, i, x, y, X, Y);
 }
 template <typename V>
 struct Bwd {  // grad^T = -div: vx at x and x-1, vy at y and y-1
@@ -311,9 +332,7 @@ struct Bwd {  // grad^T = -div: vx at x and x-1, vy at y and y-1
     }
 };
 template <typename V>
-__device__ __forceinline__ Bwd<V> load_bwd(const V* vx, const V* vy, size_t i, long long m, int X, int Y) {
-    int x, y;
-    split_m(m, X, x, y);
+__device__ __forceinline__ Bwd<V> load_bwd_xy(const V* vx, const V* vy, size_t i, int x, int y, int X, int Y) {
     Bwd<V> b;
     b.hxc = x < X - 1;
     b.hxl = x > 0;
@@ -324,6 +343,12 @@ __device__ __forceinline__ Bwd<V> load_bwd(const V* vx, const V* vy, size_t i, l
     b.yc = vy[i];
     b.yu = vy[b.hyu ? i - X : i];
     return b;
+}
+template <typename V>
+__device__ __forceinline__ Bwd<V> load_bwd(const V* vx, const V* vy, size_t i, long long m, int X, int Y) {
+    int x, y;
+    split_m(m, X, x, y);
+    return load_bwd_xy(vx, vy, i, x, y, X, Y);
 }
 
 // ------------------------------------------------------------------ grid ops
@@ -527,8 +552,11 @@ k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const floa
             for (int u = 0; u < U; ++u) {
                 const int x = j + TP * (k0 + u);
                 if constexpr (INV_IN) {
-                    in[u] = op.load_nw(b, base + x, (long long)y * N + x);
+                    if constexpr (OpLoadNwXY<Op>::value) in[u] = op.load_nw_xy(b, base + x, x, y);
+                    else in[u] = op.load_nw(b, base + x, (long long)y * N + x);
                     in[u].y = row[x];
+                } else if constexpr (OpLoadXY<Op>::value) {
+                    in[u] = op.load_xy(b, base + x, x, y);
                 } else {
                     in[u] = op.load(b, base + x, (long long)y * N + x);
                 }
@@ -957,6 +985,13 @@ struct OpTvS {
         v.d = deapo[m];
         return v;
     }
+    __device__ In load_nw_xy(int, size_t i, int x, int y) const {
+        In v;
+        if (MODE != 2) v.g = load_bwd_xy(rx, ry, i, x, y, X, Y);
+        if (MODE == 2) v.pp = p[i];
+        v.d = deapo[(size_t)y * X + x];
+        return v;
+    }
     __device__ In load(int b, size_t i, long long m) const {
         In v = load_nw(b, i, m);
         v.y = w[i];
@@ -1002,6 +1037,7 @@ struct OpTvGradNorm {  // ||grad p||^2 per channel
     struct In { Fwd<V> f; };
     __device__ bool enabled(int b) const { return us[b].active; }
     __device__ In load(int, size_t i, long long m) const { return In{load_fwd(p, i, m, X, Y)}; }
+    __device__ In load_xy(int, size_t i, int x, int y) const { return In{load_fwd_xy(p, i, x, y, X, Y)}; }
     __device__ void apply(int, size_t, long long, const In& v, double (&acc)[2]) const {
         const V gx = v.f.gx(), gy = v.f.gy();
         acc[0] += (double)(gx.x * gx.x + gy.x * gy.x);
@@ -1037,9 +1073,13 @@ struct OpTvStepS {
         v.y = w[i];
         return v;
     }
-    __device__ In load_nw(int, size_t i, long long m) const {
+    __device__ In load_nw(int b, size_t i, long long m) const {
         int x, y;
         split_m(m, X, x, y);
+        return load_nw_xy(b, i, x, y);
+    }
+    __device__ In load_nw_xy(int, size_t i, int x, int y) const {
+        const long long m = (long long)y * X + x;
         In v;
         v.hr = x < X - 1;
         v.hd = y < Y - 1;
@@ -1110,6 +1150,9 @@ struct OpTvShrink {
     __device__ bool enabled(int) const { return true; }
     __device__ In load(int, size_t i, long long m) const {
         return In{load_fwd(u, i, m, X, Y), bx[i], by[i], deapo[m]};
+    }
+    __device__ In load_xy(int, size_t i, int x, int y) const {
+        return In{load_fwd_xy(u, i, x, y, X, Y), bx[i], by[i], deapo[(size_t)y * X + x]};
     }
     __device__ void apply(int b, size_t i, long long m, const In& in, double (&acc)[1]) const {
         w[i] = value(b, i, m, in, acc);
