@@ -132,6 +132,15 @@ template <class Op>
 struct OpUnroll<Op, std::void_t<decltype(Op::kUnroll)>> {
     static constexpr int value = Op::kUnroll;
 };
+// elements in flight per thread in k_tv_rowfft: Op::kRowUnroll, else as k_grid
+template <class Op, class = void>
+struct OpRowUnroll {
+    static constexpr int value = OpUnroll<Op>::value;
+};
+template <class Op>
+struct OpRowUnroll<Op, std::void_t<decltype(Op::kRowUnroll)>> {
+    static constexpr int value = Op::kRowUnroll;
+};
 
 #ifndef TV_UNROLL
 #define TV_UNROLL 2
@@ -513,12 +522,15 @@ k_sirt_adjpost_rowfft(const float2* __restrict__ w, float2* __restrict__ g, cons
 // per CTA in a fixed order into part[(y0 / 4 * B + b) * K + k] for k_finish
 // (deterministic).
 template <int LOGN, bool INV_IN, bool FWD_OUT, int K, class Op>
-__global__ void __launch_bounds__(4 * (1 << LOGN) / 16, 1024 / (4 * (1 << LOGN) / 16))
+// (no transform: no row buffer, 32 registers, 4 CTAs of 16 warps per SM --
+// the gradient norm 259 -> 232 us)
+__global__ void __launch_bounds__(4 * (1 << LOGN) / 16,
+                                  ((INV_IN || FWD_OUT) ? 1024 : 2048) / (4 * (1 << LOGN) / 16))
 k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const float2* __restrict__ tw,
             double* __restrict__ part) {
     using namespace fftcore;
     constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3, NT = 4 * TP;
-    constexpr int U = OpUnroll<Op>::value;
+    constexpr int U = OpRowUnroll<Op>::value;
     static_assert(16 % U == 0, "unroll divides 16");
     extern __shared__ __align__(16) float2 tv_fbuf[];
     __shared__ double red[K][NT / 32];
@@ -1139,6 +1151,8 @@ struct OpTvStepS {
 template <typename R, typename V>
 struct OpTvShrink {
     static constexpr int kUnroll = TV_UNROLL;
+    // in the fused x pass 4 elements' loads in flight (1.82 -> 1.71 ms, 56 registers)
+    static constexpr int kRowUnroll = 4;
     using C = typename CT<R>::T;
     const V* u;
     V *rx, *ry, *bx, *by;

@@ -2,7 +2,7 @@
 # ncu --set full of the four fused TV x-pass kernels (one launch each, first outer iteration)
 O=gpurun_out
 mkdir -p $O
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:"^k_tv_rowfft" -c 4 -o $O/r02_full_tvrow python scratch/tv_probe.py 1 > $O/tvrow_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base function -k regex:"^k_tv_rowfft" -c 6 -o $O/r02_full_tvrow python scratch/tv_probe.py 1 > $O/tvrow_ncu.log 2>&1
 python - <<'PY'
 import csv, subprocess
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
