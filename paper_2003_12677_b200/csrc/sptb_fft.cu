@@ -312,70 +312,6 @@ k_fft1r_fwd(const float* __restrict__ in, int cplx, long long n, long long u0, i
     }
 }
 
-// q[perm[t * N + p]][b] -> inverse FFT along p, * scale -> caller slices
-template <int LOGN>
-__global__ void __launch_bounds__(FBG * (1 << LOGN) / 16, 2)
-k_fft1r_inv(const float2* __restrict__ q, int B, const int* __restrict__ perm, const float2* __restrict__ tw,
-            float scale, float* __restrict__ out, int cplx, long long n, long long u0, int nb, int T) {
-    constexpr int N = 1 << LOGN, TP = N / 16, R3 = N / 256, NB3 = 16 / R3;
-    extern __shared__ __align__(16) float2 fbuf[];
-    const int t = blockIdx.y, b0 = blockIdx.x * FBG;
-    const int b = threadIdx.x / TP, j = threadIdx.x % TP;
-    float2* buf = fbuf + b * N;
-    const int* pr = perm + (long long)t * N;
-    constexpr int NI = N / (FBG * TP);  // = 4: all gathers in flight before any shared store
-    float4 glo[NI], ghi[NI];
-#pragma unroll
-    for (int k = 0; k < NI; ++k) {
-        const float4* src =
-            reinterpret_cast<const float4*>(q + (size_t)__ldg(pr + threadIdx.x + k * FBG * TP) * B + b0);
-        glo[k] = __ldg(src);
-        ghi[k] = __ldg(src + 1);
-    }
-#pragma unroll
-    for (int k = 0; k < NI; ++k) {
-        const int i = threadIdx.x + k * FBG * TP;
-        const float4 lo = glo[k], hi = ghi[k];
-        const int si = swz4(i);
-        fbuf[si] = make_float2(lo.x, lo.y);
-        fbuf[N + si] = make_float2(lo.z, lo.w);
-        fbuf[2 * N + si] = make_float2(hi.x, hi.y);
-        fbuf[3 * N + si] = make_float2(hi.z, hi.w);
-    }
-    __syncthreads();
-    float2 v[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = buf[swz4(j + TP * r)];
-    dft16<true>(v);
-    __syncthreads();  // stage 1 reads done before fft16_stages overwrites buf
-    fft16_stages<LOGN, true>(v, buf, j, tw);
-    if (b0 + b >= nb) return;
-    const long long plane = (long long)T * N;
-    const long long u = u0 + b0 + b;
-    float* pa;
-    float* pb = nullptr;
-    if (cplx) {
-        pa = out + (u * plane + (long long)t * N) * 2;
-    } else {
-        pa = out + (2 * u) * plane + (long long)t * N;
-        if (2 * u + 1 < n) pb = out + (2 * u + 1) * plane + (long long)t * N;
-    }
-#pragma unroll
-    for (int c = 0; c < NB3; ++c)
-#pragma unroll
-        for (int r = 0; r < R3; ++r) {
-            const int i = j + c * TP + 256 * r;
-            const float2 z = v[c * R3 + r];
-            if (cplx) {
-                reinterpret_cast<float2*>(pa)[i] = make_float2(z.x * scale, z.y * scale);
-            } else {
-                pa[i] = z.x * scale;
-                if (pb) pb[i] = z.y * scale;
-            }
-        }
-}
-
-
 // ---------------------------------------------------------------------------
 // 2-D inverse FFT of the gridded batch G [b][y][x] (after S) fused with the
 // deapodization and the unpack to the caller's real slice pairs.  cuFFT's
@@ -1539,18 +1475,9 @@ int fwd_launch(sptb_plan* p, const void* in, int fmt, int64_t n, int64_t u0, int
 template <int LOGN>
 int inv_launch(sptb_plan* p, const void* q, int B, void* out, int fmt, int64_t n, int64_t u0, int nb,
                cudaStream_t st) {
+    // (a register radix-16 inverse, as the forward, measured slower than the
+    // Stockham kernel on the gathered input and was removed)
     const size_t sm = sizeof(float2) * FBG * (1 << LOGN);
-    if constexpr (LOGN >= 9) {
-        if (switches().fft1_r16_inv) {  // measured: the Stockham inverse is faster (gathered input)
-            constexpr int NT = FBG * (1 << LOGN) / 16;
-            SPTB_CUDA(set_smem_once((const void*)k_fft1r_inv<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
-            k_fft1r_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), NT, sm, st>>>(
-                (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,
-                (fmt & SPTB_FMT_COMPLEX) ? 1 : 0, n, u0, nb, p->T);
-            SPTB_LAUNCHED();
-            return SPTB_OK;
-        }
-    }
     SPTB_CUDA(set_smem_once((const void*)k_fft1_inv<LOGN>, (int)sm, SPTB_FFT_CARVEOUT));
     k_fft1_inv<LOGN><<<dim3((unsigned)((nb + FBG - 1) / FBG), (unsigned)p->T), FT, sm, st>>>(
         (const float2*)q, B, p->shp.perm, (const float2*)p->tw1, 1.0f / (float)p->P, (float*)out,

@@ -138,10 +138,9 @@ struct SSeg {
 struct Switches {
     bool no_tma = false, no_fused_fft1 = false, no_fused_fft2 = false;
     bool fft2_no_persist = false, fft2_no_bulk = false;
-    bool fft1_stockham = false, fft1_no_bulk = false, fft1_r16_inv = false;
+    bool fft1_stockham = false, fft1_no_bulk = false;
     bool fft1_inv_gather = false, fft1_fwd_rows = false, fft1_perm = false;
     bool sirt_unfused = false, xpass_unfused = false, spmm_rows = false, no_graph = false;
-    int sh_grid = 0;       // S^H launch grid override (0: default)
     int pipe_chunks = 0;   // host pipeline chunks per call (0: default)
 };
 const Switches& switches();

@@ -35,7 +35,6 @@ void reload_switches() {
     s.fft2_no_bulk = env_on("SPTB_FFT2_NO_BULK");
     s.fft1_stockham = env_on("SPTB_FFT1_STOCKHAM");
     s.fft1_no_bulk = env_on("SPTB_FFT1_NO_BULK");
-    s.fft1_r16_inv = env_on("SPTB_FFT1_R16_INV");
     s.fft1_inv_gather = env_on("SPTB_FFT1_INV_GATHER");
     s.fft1_fwd_rows = env_on("SPTB_FFT1_FWD_ROWS");
     s.fft1_perm = env_on("SPTB_FFT1_PERM");

@@ -102,20 +102,16 @@ def test_fused_fft2_unpack_matches_cufft_path(sb, n, T, nx, ny):
 
 
 def test_fused_fft1_stockham_variant(sb):
-    """n_p >= 512: the forward runs the register radix-16 kernel and the
-    inverse the Stockham kernel by default; both have the other variant."""
+    """n_p >= 512: the forward runs the register radix-16 kernel by default
+    (the Stockham kernel below 512); both give the same iradon."""
     import torch
     ops = _ops(sb, 512, 30)
     sino = torch.randn(8, 30, 512, device="cuda")
-    img = torch.randn(8, 512, 512, device="cuda")
-    a, ra = ops.iradon(sino), ops.radon(img)
+    a = ops.iradon(sino)
     with _env("SPTB_FFT1_STOCKHAM", "1"):
         b = ops.iradon(sino)
-    with _env("SPTB_FFT1_R16_INV", "1"):
-        rb = ops.radon(img)
     torch.cuda.synchronize()
     assert rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
-    assert rel(ra.cpu().numpy(), rb.cpu().numpy()) < 1e-5
 
 
 def test_sh_tma_matches_ldgsts_kernel(sb):
@@ -298,3 +294,24 @@ def test_cgls_fused_passes_match_unfused(sb, n, T, nx, ny, nonneg):
     # orthogonality; fused and unfused alike): the early residuals agree
     for r, r3 in zip(rep, rep3):
         np.testing.assert_allclose(r.residual_history[:4], r3.residual_history[:4], rtol=1e-4)
+
+
+@pytest.mark.parametrize("algo,kind", [("sirt", "hamming"), ("cgls", "none"), ("tv", "none")])
+def test_graph_replay_matches_eager(sb, algo, kind):
+    """Iterations 2.. replay a CUDA graph captured from iteration 1; the same
+    solve issued eagerly (SPTB_NO_GRAPH) launches the same kernels in the
+    same order: bitwise identical reconstructions and histories."""
+    import torch
+    from paper_2003_12677_b200.solvers import solve_batch
+    ops = _ops(sb, 512, 96, kind)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    sino = ops.radon(torch.rand(6, 512, 512, device="cuda", generator=g))
+    cfg = sb.SolverConfig(algorithm=algo, max_iter=5)
+    rec, rep, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    with _env("SPTB_NO_GRAPH", "1"):
+        rec2, rep2, _ = solve_batch(sino, ops, cfg, raise_on_failure=False)
+    a = np.asarray(rec.cpu() if hasattr(rec, "cpu") else rec)
+    b = np.asarray(rec2.cpu() if hasattr(rec2, "cpu") else rec2)
+    np.testing.assert_array_equal(a, b)
+    for r, r2 in zip(rep, rep2):
+        assert r.residual_history == r2.residual_history
