@@ -108,3 +108,40 @@ def test_sirt5_headline_batch(env):
         assert e < 1e-3, (k, e)
         eh = parity.rel_l2(reps[k].residual_history, hist)
         assert eh < 1e-3, (k, eh)
+
+
+def test_headline_batch_properties(env):
+    """Size-independent properties on all 64 slices of the production batch
+    (every slot, not only the oracle-checked ones): adjointness of the radon
+    pair <s, A u> = <A^H s, u> per slice, linearity of A, and slot
+    independence -- a pair's gridrec does not depend on its batch slot
+    (the stack rolled by 6 pairs gives the same slices bit for bit: fixed
+    per-unit reduction order), and slice 37 alone (other kernels: a
+    one-unit launch) agrees to rounding."""
+    sb, torch = env["sb"], env["torch"]
+    ops = sb.build_operators(env["geom"], filter_kind="ramlak", max_batch=32)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(21)
+    u = torch.rand(NZ, N_P, N_P, device=dev, generator=g)
+    s = torch.randn(NZ, N_T, N_P, device=dev, generator=g)
+    au = ops.radon(u)
+    ahs = ops.radon_adjoint(s)
+    lhs = (s.double() * au.double()).sum(dim=(1, 2))
+    rhs = (ahs.double() * u.double()).sum(dim=(1, 2))
+    # complex64 kernels; s has random signs, so <s, A u> ~ sqrt(N) |terms| and
+    # its relative rounding is ~1e-5 (the complex128 build meets 1e-8:
+    # test_gpu_operators.py::test_adjoint_identity_and_linearity)
+    err = ((lhs - rhs).abs() / lhs.abs().clamp_min(1e-30)).max().item()
+    assert err < 1e-4, err
+    v = torch.rand(NZ, N_P, N_P, device=dev, generator=g)
+    lin = ops.radon(0.75 * u - 1.5 * v)
+    ref = 0.75 * au - 1.5 * ops.radon(v)
+    assert ((lin - ref).norm() / ref.norm()).item() < 1e-6
+    rec = ops.iradon(s)
+    rolled = ops.iradon(torch.roll(s, 12, dims=0).contiguous())
+    one = ops.iradon(s[37:38].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(torch.roll(rolled, -12, dims=0), rec)
+    # a lone slice is packed with a zero partner and runs the one-unit
+    # kernels: rounding only
+    assert ((one[0] - rec[37]).norm() / rec[37].norm()).item() < 1e-5
