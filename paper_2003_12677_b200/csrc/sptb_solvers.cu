@@ -1313,17 +1313,6 @@ k_spec(RV* __restrict__ rh, const typename CT<R>::T* __restrict__ qh,
     }
 }
 
-template <typename A, typename Bt>
-__global__ void k_convert(const A* __restrict__ src, Bt* __restrict__ dst, long long n) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        Bt o;
-        o.x = src[i].x;
-        o.y = src[i].y;
-        dst[i] = o;
-    }
-}
-
 // ------------------------------------------------------------------ scalar kernels
 // A, C -> per-channel squared weighted norms
 // (clamps rounding negatives to 0 but lets NaN through, like the reference's sums)
