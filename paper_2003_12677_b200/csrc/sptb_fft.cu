@@ -1198,16 +1198,26 @@ int log2_fft(long long n) {
     return l;
 }
 
+// W_n^k for k < n, then (n >= 256) the stage tables of fft16_stages_tab:
+// T2[r][m] = W_n^(m (n/256) r) (16 x 16) and T3[r][m] = W_n^(m r) (n/256 x 256)
 const float2* twiddles(sptb_plan* p, int logn) {
     if (!p->twn[logn]) {
         const int n = 1 << logn;
+        auto w = [n](long long k) {
+            const double a = -2.0 * M_PI * (double)(k % n) / (double)n;
+            return make_float2((float)std::cos(a), (float)std::sin(a));
+        };
         std::vector<float2> h(n);
-        for (int k = 0; k < n; ++k) {
-            const double a = -2.0 * M_PI * (double)k / (double)n;
-            h[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+        for (int k = 0; k < n; ++k) h[k] = w(k);
+        if (n >= 256) {
+            const int r3 = n / 256;
+            for (int r = 0; r < 16; ++r)
+                for (int m = 0; m < 16; ++m) h.push_back(w((long long)m * (n / 256) * r));
+            for (int r = 0; r < r3; ++r)
+                for (int m = 0; m < 256; ++m) h.push_back(w((long long)m * r));
         }
-        if (cudaMalloc(&p->twn[logn], sizeof(float2) * n) != cudaSuccess) return nullptr;
-        if (cudaMemcpy(p->twn[logn], h.data(), sizeof(float2) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+        if (cudaMalloc(&p->twn[logn], sizeof(float2) * h.size()) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(p->twn[logn], h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             return nullptr;
     }
     return (const float2*)p->twn[logn];

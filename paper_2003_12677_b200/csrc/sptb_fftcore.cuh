@@ -224,5 +224,55 @@ __device__ __forceinline__ void fft16_stages_pre(float2* v, float2* buf, int j, 
     }
 }
 
+// fft16_stages with the stage-2/3 twiddle powers read from the plan's
+// per-LOGN tables instead of built by products (one-pass kernels that cannot
+// keep StageTwiddles in registers): tw + N holds T2[r][m] = W_N^(m (N/256) r)
+// (16 x 16, r-major: a warp's lanes read 16 consecutive entries) and
+// tw + N + 256 holds T3[r][m] = W_N^(m r) (R3 x 256), rounded from double.
+// Measured against the products: SIRT's update pass 0.881 -> 0.854 ms, the
+// TV passes within 1% (the one-pass kernels are bound by memory latency and
+// the exchange barriers, not by the twiddle arithmetic)
+template <int LOGN, bool INV>
+__device__ __forceinline__ void fft16_stages_tab(float2* v, float2* buf, int j, const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, T = N / 16, R3 = N / 256, NB3 = 16 / R3;
+    const float2* t2 = tw + N;
+    const float2* t3 = tw + N + 256;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4(16 * j + r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        const float2 x = buf[swz4(j + T * r)];
+        if (r) {
+            float2 w = __ldg(t2 + r * 16 + (j & 15));
+            if (INV) w.y = -w.y;
+            v[r] = cmul(x, w);
+        } else {
+            v[r] = x;
+        }
+    }
+    dft16<INV>(v);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[swz4((j >> 4) * 256 + (j & 15) + 16 * r)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NB3; ++c) {
+        const int jj = j + c * T;
+#pragma unroll
+        for (int r = 0; r < R3; ++r) {
+            const float2 x = buf[swz4(jj + (N / R3) * r)];
+            if (r) {
+                float2 w = __ldg(t3 + r * 256 + (jj & 255));
+                if (INV) w.y = -w.y;
+                v[c * R3 + r] = cmul(x, w);
+            } else {
+                v[c * R3 + r] = x;
+            }
+        }
+        dft_r<R3, INV>(v + c * R3);
+    }
+}
+
 }  // namespace fftcore
 }  // namespace sptb

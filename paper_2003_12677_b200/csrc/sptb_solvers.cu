@@ -444,7 +444,7 @@ k_sirt_update_rowfft(float2* __restrict__ u, const float2* __restrict__ g, float
         v[r] = make_float2(x.x * d, x.y * d);
     }
     dft16<false>(v);
-    fft16_stages<LOGN, false>(v, sirt_fbuf + rb * N, j, tw);
+    fft16_stages_tab<LOGN, false>(v, sirt_fbuf + rb * N, j, tw);
 #pragma unroll
     for (int q = 0; q < NB3; ++q)
 #pragma unroll
@@ -475,7 +475,7 @@ k_sirt_adjpost_rowfft(const float2* __restrict__ w, float2* __restrict__ g, cons
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = w[base + j + TP * r];
     dft16<true>(v);
-    fft16_stages<LOGN, true>(v, sirt_fbuf + rb * N, j, tw);
+    fft16_stages_tab<LOGN, true>(v, sirt_fbuf + rb * N, j, tw);
     double acc[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int q = 0; q < NB3; ++q)
@@ -545,7 +545,7 @@ k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const floa
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = w[base + j + TP * r];
         dft16<true>(v);
-        fft16_stages<LOGN, true>(v, row, j, tw);
+        fft16_stages_tab<LOGN, true>(v, row, j, tw);
         __syncthreads();  // stage 3 read other lanes' slots
 #pragma unroll
         for (int q = 0; q < NB3; ++q)
@@ -591,7 +591,7 @@ k_tv_rowfft(Op op, float2* __restrict__ w, long long M, int Y, int B, const floa
         for (int r = 0; r < 16; ++r) v[r] = row[j + TP * r];  // own slots
         __syncthreads();  // fft16_stages overwrites other lanes' slots
         dft16<false>(v);
-        fft16_stages<LOGN, false>(v, row, j, tw);
+        fft16_stages_tab<LOGN, false>(v, row, j, tw);
 #pragma unroll
         for (int q = 0; q < NB3; ++q)
 #pragma unroll
