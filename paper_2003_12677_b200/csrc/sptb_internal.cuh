@@ -142,6 +142,7 @@ struct Switches {
     bool fft1_inv_gather = false, fft1_fwd_rows = false, fft1_perm = false;
     bool sirt_unfused = false, xpass_unfused = false, spmm_rows = false, no_graph = false;
     int pipe_chunks = 0;   // host pipeline chunks per call (0: default)
+    std::vector<int> pipe_sizes;  // explicit host pipeline chunk sizes in units (A/B)
 };
 const Switches& switches();
 void reload_switches();
