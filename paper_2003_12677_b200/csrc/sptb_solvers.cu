@@ -2376,6 +2376,37 @@ int solve_typed(sptb_plan* p, const sptb_solver_config& cfg, const void* sino, i
 
 using namespace sptb;
 
+// Every solver grid pass multiplies by the deapodization plane (M reals),
+// re-read once per unit: 32 x 16.8 MB per pass at 2048^2 when the streaming
+// W / u / g traffic evicts it from L2 between units.  Pin it in the L2
+// persisting carve-out for the solver stream's kernels (captured into the
+// iteration graphs with the launches).  SPTB_NO_L2_PERSIST: off (A/B).
+static void persist_deapo(sptb_plan* p) {
+    const char* off = getenv("SPTB_NO_L2_PERSIST");
+    if ((off && off[0] && off[0] != '0') || !p->deapo) return;
+    int maxp = 0, maxw = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device);
+    const size_t bytes = (size_t)p->M * (p->csize / 2);
+    if (maxp <= 0 || maxw <= 0) return;
+    const size_t win = std::min(bytes, (size_t)maxw);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    const size_t want = std::min(win, (size_t)maxp);
+    if (cur < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.base_ptr = p->deapo;
+    a.accessPolicyWindow.num_bytes = win;
+    a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)std::max(cur, want) / (double)win);
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(p->solver_stream, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess)
+        cudaGetLastError();
+}
+
 extern "C" int sptb_solve(sptb_plan* p, const sptb_solver_config* cfg, const void* sino,
                           int32_t in_fmt, void* rec, int32_t out_fmt, int64_t n, double* hist,
                           int32_t* iters, int32_t* converged, int32_t* status) {
@@ -2393,6 +2424,7 @@ extern "C" int sptb_solve(sptb_plan* p, const sptb_solver_config* cfg, const voi
     if (!p->solver_stream) {
         SPTB_CUDA(cudaStreamCreateWithFlags(&p->solver_stream, cudaStreamNonBlocking));
         for (auto& e : p->solver_join) SPTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        persist_deapo(p);
     }
     cudaStream_t caller = p->stream;
     SPTB_CUDA(cudaEventRecord(p->solver_join[0], caller));
