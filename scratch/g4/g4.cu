@@ -73,6 +73,35 @@ __global__ void __launch_bounds__(256) k_ldg(const float4* __restrict__ x, const
     if (acc == 12345.f) out[0] = acc;
 }
 
+// warp per row: each LDG touches one 128-byte line (LDG.32, 2 per row) or two (LDG.64, 1 per row)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_ldgw(const float* __restrict__ x, const int* __restrict__ idx, long long n,
+                                              float* out) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * 8, w0 = blockIdx.x * 8LL + (threadIdx.x >> 5);
+    float acc = 0.f;
+    for (long long j0 = w0 * 8; j0 < n; j0 += warps * 8) {
+        if (MODE == 0) {
+            float a[8], b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float* r = x + (size_t)idx[j0 + u] * 64;
+                a[u] = __ldg(r + lane);
+                b[u] = __ldg(r + 32 + lane);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += a[u] + b[u];
+        } else {
+            float2 a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldg(reinterpret_cast<const float2*>(x + (size_t)idx[j0 + u] * 64) + lane);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += a[u].x + a[u].y;
+        }
+    }
+    if (acc == 12345.f) out[0] = acc;
+}
+
 extern "C" int g4_run(const void* x, long long nrows, const int* idx, long long n, int mode, int grid, float* ms) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
@@ -100,7 +129,9 @@ extern "C" int g4_run(const void* x, long long nrows, const int* idx, long long 
     for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
         if (mode == 0) k_g4<<<grid, 256, sm>>>(tm, idx, n, out);
-        else k_ldg<<<grid, 256>>>((const float4*)x, idx, n, out);
+        else if (mode == 1) k_ldg<<<grid, 256>>>((const float4*)x, idx, n, out);
+        else if (mode == 2) k_ldgw<0><<<grid, 256>>>((const float*)x, idx, n, out);
+        else k_ldgw<1><<<grid, 256>>>((const float*)x, idx, n, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
     }

@@ -15,7 +15,7 @@ n = (nnz // 64) * 64
 idx = torch.tensor(ci[:n], dtype=torch.int32, device="cuda")
 x = torch.randn(cols, 64, device="cuda")  # 256-byte rows
 ms = C.c_float()
-for mode, name in ((1, "ldg"), (0, "gather4")):
+for mode, name in ((1, "ldg128 half-warp/row"), (2, "ldg32 warp/row 1 line/instr"), (3, "ldg64 warp/row 2 lines/instr")):
     for grid in (148 * 2, 148 * 4, 148 * 8):
         rc = lib.g4_run(C.c_void_p(x.data_ptr()), C.c_longlong(cols), C.c_void_p(idx.data_ptr()), C.c_longlong(n), mode, grid, C.byref(ms))
         print(f"{name} grid {grid}: rc {rc}  {ms.value:.3f} ms  {n * 256 / ms.value / 1e6:.0f} GB/s gathered", flush=True)
