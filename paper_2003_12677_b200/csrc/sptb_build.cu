@@ -204,8 +204,8 @@ int build_typed(sptb_plan* p, const BuildArgs& a) {
     S.cols = N;
     S.nnz = nnz;
     SPTB_CUDA(cudaMalloc(&S.row_ptr, sizeof(int) * (M + 1)));
-    SPTB_CUDA(cudaMalloc(&S.col, sizeof(int) * nn));
-    SPTB_CUDA(cudaMalloc(&S.val, sizeof(C) * nn));
+    SPTB_CUDA(cudaMalloc(&S.col, sizeof(int) * (nn + 4)));  // +4: 16-byte bulk-copy slack (S kernel staging)
+    SPTB_CUDA(cudaMalloc(&S.val, sizeof(C) * (nn + 4)));
     int *keys_out = nullptr, *idx_in = nullptr, *idx_out = nullptr, *rcnt = nullptr;
     SPTB_CUDA(cudaMalloc(&keys_out, sizeof(int) * nn));
     SPTB_CUDA(cudaMalloc(&idx_in, sizeof(int) * nn));
@@ -492,7 +492,7 @@ int build_patches(sptb_plan* p, const BuildArgs& a) {
     SPTB_CUDA(cudaMalloc(&sp.items, sizeof(int4) * std::max<size_t>(items.size(), 1)));
     SPTB_CUDA(cudaMalloc(&sp.perm, sizeof(int) * N));
     SPTB_CUDA(cudaMalloc(&sp.order, sizeof(int) * N));
-    SPTB_CUDA(cudaMalloc(&sp.s_colp, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    SPTB_CUDA(cudaMalloc(&sp.s_colp, sizeof(int) * (std::max<int64_t>(nnz, 1) + 4)));
     if (!items.empty())
         SPTB_CUDA(cudaMemcpy(sp.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
     if (!item_perm.empty()) {
@@ -742,7 +742,7 @@ int fold_filter(sptb_plan* p) {
     }
     SPTB_TRY(upload_weights(p));
     if (p->w_len == 0) return SPTB_OK;
-    SPTB_CUDA(cudaMalloc(&p->SW_val, cs * (nnz > 0 ? nnz : 1)));
+    SPTB_CUDA(cudaMalloc(&p->SW_val, cs * ((nnz > 0 ? nnz : 1) + 4)));
     if (nnz == 0) return SPTB_OK;
     // weights multiply in double like the reference's folded build (gridding.py:146-152)
     // -- float plans round the folded value once.

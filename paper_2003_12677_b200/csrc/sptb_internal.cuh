@@ -131,6 +131,7 @@ struct SSeg {
     int4* tiles = nullptr;  // {row begin, row end, first pair record, pair records}
     int* longs = nullptr;   // long row ids, longest first
     unsigned long long* pairs = nullptr;  // per tile, its rows by length in pairs (packed)
+    int4* tile_e = nullptr;  // per tile {first entry, entries, first pair, pairs} (L2 prefetch of a later tile)
 };
 
 // Path-selection switches (tests and A/B measurements only): read from the

@@ -472,7 +472,7 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->stage_in, p->stage_out, p->red, p->fft_work,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
                     p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->sseg.tiles,
-                    p->sseg.longs, p->sseg.pairs, p->wspec_dev, p->tw1};
+                    p->sseg.longs, p->sseg.pairs, p->sseg.tile_e, p->wspec_dev, p->tw1};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->twn)
