@@ -740,6 +740,7 @@ int fold_filter(sptb_plan* p) {
         cudaFree(p->SW_val);
         p->SW_val = nullptr;
     }
+    p->sseg.pval_ok[1] = false;  // the S kernel's padded copy of S diag(w) is stale
     SPTB_TRY(upload_weights(p));
     if (p->w_len == 0) return SPTB_OK;
     SPTB_CUDA(cudaMalloc(&p->SW_val, cs * ((nnz > 0 ? nnz : 1) + 4)));

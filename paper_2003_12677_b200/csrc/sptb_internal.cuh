@@ -132,6 +132,13 @@ struct SSeg {
     int* longs = nullptr;   // long row ids, longest first
     unsigned long long* pairs = nullptr;  // per tile, its rows by length in pairs (packed)
     int4* tile_e = nullptr;  // per tile {first entry, entries, first pair, pairs} (L2 prefetch of a later tile)
+    // the copy of S the kernel reads: rows start on even entries (zero pads),
+    // columns [0] sample order / [1] s', values [0] S / [1] S diag(w)
+    int* prp = nullptr;
+    int64_t pnnz = 0;
+    int* pcol[2] = {nullptr, nullptr};
+    void* pval[2] = {nullptr, nullptr};
+    bool pcol_ok[2] = {false, false}, pval_ok[2] = {false, false};
 };
 
 // Path-selection switches (tests and A/B measurements only): read from the

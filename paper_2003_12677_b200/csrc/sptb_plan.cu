@@ -472,7 +472,8 @@ int sptb_plan_destroy(sptb_plan* p) {
                     p->stage_in, p->stage_out, p->red, p->fft_work,
                     p->shp.items, p->shp.rp, p->shp.meta, p->shp.perm, p->shp.order,
                     p->shp.s_colp, p->shp.sval, p->shp.item_perm, p->sseg.tiles,
-                    p->sseg.longs, p->sseg.pairs, p->sseg.tile_e, p->wspec_dev, p->tw1};
+                    p->sseg.longs, p->sseg.pairs, p->sseg.tile_e, p->sseg.prp, p->sseg.pcol[0], p->sseg.pcol[1],
+                    p->sseg.pval[0], p->sseg.pval[1], p->wspec_dev, p->tw1};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (void* b : p->twn)

@@ -47,6 +47,9 @@ constexpr int SEG_HALVES = SEG_THREADS / 16;
 constexpr int SEG_TR = SEG_TR_;   // rows per tile (shared output tile)
 constexpr int SEG_W = SEG_W_;     // nonzeros per tile (staged metadata)
 constexpr int SEG_LONG = 128;     // longer rows: one CTA per row
+#ifndef SEG_ALIGN2
+#define SEG_ALIGN2 1                 // rows laid out on even entries (padded copy of S)
+#endif
 #ifndef SEG_UNR_
 #define SEG_UNR_ 8
 #endif
@@ -97,10 +100,26 @@ struct Acc {
     template <int K>
     __device__ __forceinline__ void exact(const int* s_col, const float2* s_val, const float4* xl, int j0) {
         float4 q[K];
+#if SEG_ALIGN2
+        // rows start on even entries: columns two per 8-byte load, values two per 16-byte load
+#pragma unroll
+        for (int u = 0; u < K; u += 2) {
+            const int2 c = *reinterpret_cast<const int2*>(s_col + j0 + u);
+            q[u] = ldg_nc4(xl + (size_t)c.x * (SEG_BB / 2));
+            if (u + 1 < K) q[u + 1] = ldg_nc4(xl + (size_t)c.y * (SEG_BB / 2));
+        }
+#pragma unroll
+        for (int u = 0; u < K; u += 2) {
+            const float4 v = *reinterpret_cast<const float4*>(s_val + j0 + u);
+            mac(make_float2(v.x, v.y), q[u]);
+            if (u + 1 < K) mac(make_float2(v.z, v.w), q[u + 1]);
+        }
+#else
 #pragma unroll
         for (int u = 0; u < K; ++u) q[u] = ldg_nc4(xl + (size_t)s_col[j0 + u] * (SEG_BB / 2));
 #pragma unroll
         for (int u = 0; u < K; ++u) mac(s_val[j0 + u], q[u]);
+#endif
     }
     // the first n (< K possible, <= 0 allowed) of K positions; the others load
     // staged entry 0 with weight 0
@@ -197,7 +216,8 @@ __global__ void __launch_bounds__(SEG_THREADS, SEG_MINB_)
 k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const float2* __restrict__ val,
            const float2* __restrict__ x, float2* __restrict__ y, long long M,
            const int4* __restrict__ tiles, const unsigned long long* __restrict__ pairs,
-           const int* __restrict__ longs, int n_long, const int4* __restrict__ tile_e, int n_tiles, int pf) {
+           const int* __restrict__ longs, int n_long, const int4* __restrict__ tile_e, int n_tiles, int pf,
+           const int* __restrict__ prp) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long stage_bar;
     float4* out = reinterpret_cast<float4*>(smem);
@@ -211,7 +231,7 @@ k_spmm_seg(const int* __restrict__ row_ptr, const int* __restrict__ col, const f
     if ((int)blockIdx.x < n_long) {
         // ---- one long row: 16 contiguous pieces, summed in piece order
         const int r = longs[blockIdx.x];
-        const int e0 = row_ptr[r], len = row_ptr[r + 1] - e0;
+        const int e0 = prp[r], len = row_ptr[r + 1] - row_ptr[r];
         const int pb = e0 + (int)(((long long)len * h) / SEG_HALVES);
         const int pe = e0 + (int)(((long long)len * (h + 1)) / SEG_HALVES);
         Acc acc;
@@ -299,15 +319,22 @@ int build_seg(sptb_plan* p) {
     SSeg& s = p->sseg;
     if (s.built) return SPTB_OK;
     const int64_t M = p->S.rows;
-    std::vector<int> rp(M + 1);
-    SPTB_CUDA(cudaMemcpy(rp.data(), p->S.row_ptr, sizeof(int) * (M + 1), cudaMemcpyDeviceToHost));
+    std::vector<int> rp0(M + 1), rp(M + 1);
+    SPTB_CUDA(cudaMemcpy(rp0.data(), p->S.row_ptr, sizeof(int) * (M + 1), cudaMemcpyDeviceToHost));
+    // rp: row pointers of the copy of S the kernel reads (rows on even entries when SEG_ALIGN2)
+    rp[0] = 0;
+    for (int64_t q = 0; q < M; ++q) {
+        const int ln = rp0[q + 1] - rp0[q];
+        rp[q + 1] = rp[q] + (SEG_ALIGN2 ? ((ln + 1) & ~1) : ln);
+    }
+    if ((int64_t)rp[M] < (int64_t)rp0[M]) return fail(SPTB_ERR_STATE, "padded S overflows int32");
     std::vector<int4> tiles;
     std::vector<std::pair<int, int>> longs;
     std::vector<unsigned long long> pairs;
     std::vector<int4> tile_e;  // per tile {first entry, entries, first pair record, pair records}
     int64_t r = 0;
     while (r < M) {
-        const int len = rp[r + 1] - rp[r];
+        const int len = rp0[r + 1] - rp0[r];
         if (len > SEG_LONG) {
             longs.push_back({-len, (int)r});
             ++r;
@@ -316,16 +343,16 @@ int build_seg(sptb_plan* p) {
         const int64_t r0 = r;
         int nnz = 0;
         while (r < M && r - r0 < SEG_TR) {
-            const int ln = rp[r + 1] - rp[r];
-            if (ln > SEG_LONG || nnz + ln > SEG_W) break;
-            nnz += ln;
+            const int ln = rp0[r + 1] - rp0[r], pl = rp[r + 1] - rp[r];
+            if (ln > SEG_LONG || nnz + pl > SEG_W) break;
+            nnz += pl;
             ++r;
         }
         // the tile's rows by length (stable), paired: record = row a | row b
         // << 7 | has b << 14 | begin a << 15 | begin b << 25 | len a << 35 |
         // len b << 43 (rows, begins tile-local)
         std::vector<std::pair<int, int>> lr;
-        for (int64_t q = r0; q < r; ++q) lr.push_back({rp[q + 1] - rp[q], (int)(q - r0)});
+        for (int64_t q = r0; q < r; ++q) lr.push_back({rp0[q + 1] - rp0[q], (int)(q - r0)});
         std::stable_sort(lr.begin(), lr.end(),
                          [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first < y.first; });
         const int pb = (int)pairs.size();
@@ -347,6 +374,9 @@ int build_seg(sptb_plan* p) {
     for (size_t i = 0; i < longs.size(); ++i) lr[i] = longs[i].second;
     s.n_tiles = (int)tiles.size();
     s.n_long = (int)lr.size();
+    s.pnnz = rp[M];
+    SPTB_CUDA(cudaMalloc(&s.prp, sizeof(int) * (M + 1)));
+    SPTB_CUDA(cudaMemcpy(s.prp, rp.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice));
     SPTB_CUDA(cudaMalloc(&s.tiles, sizeof(int4) * std::max<size_t>(1, tiles.size())));
     SPTB_CUDA(cudaMalloc(&s.tile_e, sizeof(int4) * std::max<size_t>(1, tile_e.size())));
     if (!tile_e.empty())
@@ -361,6 +391,51 @@ int build_seg(sptb_plan* p) {
     if (!lr.empty())
         SPTB_CUDA(cudaMemcpy(s.longs, lr.data(), sizeof(int) * lr.size(), cudaMemcpyHostToDevice));
     s.built = true;
+    return SPTB_OK;
+}
+
+// row r's entries rp0[r] .. rp0[r+1]-1 -> positions prp[r] ..; pad slots stay zero
+template <typename T>
+__global__ void k_pad_rows(const int* __restrict__ rp0, const int* __restrict__ prp, const T* __restrict__ src,
+                           T* __restrict__ dst, long long M) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < M;
+         r += (long long)gridDim.x * blockDim.x) {
+        const int b = rp0[r], n = rp0[r + 1] - b, d = prp[r];
+        for (int k = 0; k < n; ++k) dst[d + k] = src[b + k];
+    }
+}
+
+// the kernel's copies of A's columns ([0] S.col, [1] the s' renumbering) and
+// values ([0] S.val, [1] SW_val) in the padded row layout, built on first use
+int ensure_padded(sptb_plan* p, const DevCSR& A, const void* vals, const int** pc, const float2** pv,
+                  cudaStream_t st) {
+    SSeg& s = p->sseg;
+    if (!SEG_ALIGN2) {
+        *pc = A.col;
+        *pv = (const float2*)vals;
+        return SPTB_OK;
+    }
+    const int ci = A.col == p->S.col ? 0 : (A.col == p->shp.s_colp ? 1 : -1);
+    const int vi = vals == p->S.val ? 0 : (vals == p->SW_val ? 1 : -1);
+    if (ci < 0 || vi < 0) return fail(SPTB_ERR_STATE, "S kernel: unknown column or value array");
+    const size_t n = (size_t)std::max<int64_t>(s.pnnz, 1) + 4;  // +4: bulk-copy slack
+    const unsigned grid = (unsigned)std::min<long long>((p->M + 255) / 256, 148 * 16);
+    if (!s.pcol_ok[ci]) {
+        if (!s.pcol[ci]) SPTB_CUDA(cudaMalloc(&s.pcol[ci], sizeof(int) * n));
+        SPTB_CUDA(cudaMemsetAsync(s.pcol[ci], 0, sizeof(int) * n, st));
+        k_pad_rows<int><<<grid, 256, 0, st>>>(A.row_ptr, s.prp, A.col, s.pcol[ci], p->M);
+        SPTB_LAUNCHED();
+        s.pcol_ok[ci] = true;
+    }
+    if (!s.pval_ok[vi]) {
+        if (!s.pval[vi]) SPTB_CUDA(cudaMalloc(&s.pval[vi], sizeof(float2) * n));
+        SPTB_CUDA(cudaMemsetAsync(s.pval[vi], 0, sizeof(float2) * n, st));
+        k_pad_rows<float2><<<grid, 256, 0, st>>>(A.row_ptr, s.prp, (const float2*)vals, (float2*)s.pval[vi], p->M);
+        SPTB_LAUNCHED();
+        s.pval_ok[vi] = true;
+    }
+    *pc = s.pcol[ci];
+    *pv = (const float2*)s.pval[vi];
     return SPTB_OK;
 }
 
@@ -383,9 +458,11 @@ int launch_spmm_seg(sptb_plan* p, const DevCSR& A, const void* vals, const void*
         const char* e = getenv("SPTB_SEG_PF");
         return e ? std::max(0, atoi(e)) : 888;
     }();
-    k_spmm_seg<<<grid, SEG_THREADS, SEG_SMEM, st>>>(A.row_ptr, A.col, (const float2*)vals, (const float2*)x,
-                                                  (float2*)y, p->M, s.tiles, s.pairs, s.longs, s.n_long, s.tile_e,
-                                                  s.n_tiles, pf);
+    const int* pc = nullptr;
+    const float2* pv = nullptr;
+    SPTB_TRY(ensure_padded(p, A, vals, &pc, &pv, st));
+    k_spmm_seg<<<grid, SEG_THREADS, SEG_SMEM, st>>>(A.row_ptr, pc, pv, (const float2*)x, (float2*)y, p->M, s.tiles,
+                                                  s.pairs, s.longs, s.n_long, s.tile_e, s.n_tiles, pf, s.prp);
     SPTB_LAUNCHED();
     return SPTB_OK;
 }
