@@ -39,7 +39,7 @@ constexpr int SEG_HALVES = SEG_THREADS / 16;
 #define SEG_W_ 1024
 #endif
 #ifndef SEG_EXACT_
-#define SEG_EXACT_ 10
+#define SEG_EXACT_ 9  // measured 9: 0.649, 10: 0.657, 8: 0.651, 6: 0.676 ms at c2
 #endif
 #ifndef SEG_MINB_
 #define SEG_MINB_ 4
@@ -55,6 +55,8 @@ constexpr int SEG_LONG = 128;     // longer rows: one CTA per row
 #endif
 constexpr int SEG_UNR = SEG_UNR_;  // gathers in flight per half-warp (long rows)
 constexpr int SEG_EXACT = SEG_EXACT_;  // row lengths with an exactly unrolled body
+static_assert(!SEG_ALIGN2 || SEG_EXACT >= 8 || SEG_EXACT % 2 == 0,
+              "exact chunks of longer rows must start on even entries (paired loads)");
 constexpr int SEG_BB = 32;        // complex columns (batch) of this kernel
 
 // shared memory: out tile [SEG_TR][16] float4 | cols [SEG_W] | vals [SEG_W] float2 | pair records
